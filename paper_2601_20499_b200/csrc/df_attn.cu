@@ -1,0 +1,473 @@
+// df_attn.cu -- ragged, head-aware FMHA for one Dummy Forcing layer (sm_100a).
+//
+// Replaces the per-group numpy attention of the reference
+//   engine.py:87-98   _batched_softmax / _batched_attention
+//   engine.py:111-137 _run_groups  (every group of a layer in ONE launch; each
+//                     head's output written straight to its slot)
+// and, with DF_ATTN_PROBE, the probe recompute + region reduction of
+//   profiler.py:105-129 (frame_attention_scores), profiler.py:147-170.
+//
+// Work item = (head, pair of 128-row query tiles).  Each head attends to its
+// own contiguous token range of a KV arena (cached frames + current frame), so
+// a dummy head with a 2-frame context issues 2/7 of the K/V tiles of a
+// baseline head: no masked tiles are ever loaded or multiplied.
+//
+// CTA = 12 warps (384 threads, 1 CTA/SM):
+//   warp 0      TMA producer (Q once; K and V rings)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2-3   idle (warpgroup 0 gives its registers to the softmax groups)
+//   warps 4-7   softmax / correction / epilogue for query tile 0 (rows 0-127)
+//   warps 8-11  same for query tile 1 (rows 128-255)
+// TMEM (512 cols): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [256+D, 256+2D).
+// P (bf16) overwrites the first 64 columns of its S buffer and is the A
+// operand (from TMEM) of O += P V.  MMA issue order per kv tile j:
+//   S0_j = Q0 K_j^T | O1 += P1_{j-1} V_{j-1} | S1_j = Q1 K_j^T | O0 += P0_j V_j
+// so the tensor pipe always has a GEMM queued while either softmax group works.
+// Online softmax in the log2 domain with lazy rescaling (threshold 2^8).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "df_internal.h"
+#include "df_ptx.cuh"
+
+namespace dfb {
+
+constexpr int kBM = 128;        // rows per query tile
+constexpr int kBN = 128;        // keys per kv tile
+constexpr int kWarps = 12;  // see role map above
+constexpr int kThreads = kWarps * 32;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units
+
+struct HeadParam {
+  int32_t base_row;
+  int32_t n_tok;
+  int16_t q_head;
+  int16_t o_head;
+  int16_t arena;
+  int16_t pad;
+};
+
+struct __align__(64) AttnParams {
+  CUtensorMap qmap;
+  CUtensorMap kvmap[2 * DF_MAX_ARENAS];
+  __nv_bfloat16* out;
+  const uint8_t* region_tab;
+  const uint8_t* row_sampled;
+  float* probe_rows;
+  int64_t out_ld;
+  int32_t hw;
+  int32_t d_out;
+  int32_t n_heads;
+  int32_t n_qpairs;
+  int32_t max_slots;
+  float scale_log2;
+  uint8_t head_order[DF_MAX_HEADS];
+  HeadParam heads[DF_MAX_HEADS];
+};
+
+template <int D>
+struct AttnCfg {
+  static constexpr int kStagesK = 2;
+  static constexpr int kStagesV = (D == 128) ? 2 : 3;
+  static constexpr int kBoxes = D / 64;                 // 128-byte wide TMA boxes per row
+  static constexpr int kTileBytes = kBN * D * 2;        // one [128 x D] bf16 tile
+  static constexpr int kBoxBytes = kBN * 128;           // one [128 x 64] box
+  static constexpr int kQOff = 0;
+  static constexpr int kKOff = kQOff + 2 * kTileBytes;
+  static constexpr int kVOff = kKOff + kStagesK * kTileBytes;
+  static constexpr int kBarOff = kVOff + kStagesV * kTileBytes;
+  static constexpr int kNumBars = 1 + 2 * kStagesK + 2 * kStagesV + 6;
+  static constexpr int kSmem = kBarOff + kNumBars * 8 + 16 + 1024;  // + 1 KB alignment slack
+  static constexpr uint32_t kTmemO = 256;
+};
+
+template <int D, bool kProbe>
+__global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_constant__ AttnParams p) {
+  using C = AttnCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = q_full + 1;
+  uint64_t* k_empty = k_full + C::kStagesK;
+  uint64_t* v_full = k_empty + C::kStagesK;
+  uint64_t* v_empty = v_full + C::kStagesV;
+  uint64_t* s_full = v_empty + C::kStagesV;  // [2]
+  uint64_t* p_full = s_full + 2;             // [2]
+  uint64_t* o_full = p_full + 2;             // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int rank = blockIdx.x / p.n_qpairs;
+  const int qp = blockIdx.x - rank * p.n_qpairs;
+  const int h = p.head_order[rank];
+  const HeadParam hd = p.heads[h];
+  const int n_kv = (hd.n_tok + kBN - 1) / kBN;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < C::kStagesK; ++s) {
+      mbar_init(k_full + s, 1);
+      mbar_init(k_empty + s, 1);
+    }
+    for (int s = 0; s < C::kStagesV; ++s) {
+      mbar_init(v_full + s, 1);
+      mbar_init(v_empty + s, 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(s_full + t, 1);
+      mbar_init(p_full + t, 128);
+      mbar_init(o_full + t, 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const void* kmap = &p.kvmap[2 * hd.arena];
+      const void* vmap = &p.kvmap[2 * hd.arena + 1];
+      prefetch_tmap(&p.qmap);
+      prefetch_tmap(kmap);
+      prefetch_tmap(vmap);
+      const uint64_t keep = policy_evict_last();  // K/V re-read by every q-tile pair of the head
+      const int qrow0 = hd.q_head * p.hw + qp * 2 * kBM;
+      mbar_expect_tx(q_full, 2 * C::kTileBytes);
+      for (int t = 0; t < 2; ++t)
+        for (int b = 0; b < C::kBoxes; ++b)
+          tma_load_2d(smem + C::kQOff + t * C::kTileBytes + b * C::kBoxBytes, &p.qmap, q_full, b * 64,
+                      qrow0 + t * kBM);
+      for (int j = 0; j < n_kv; ++j) {
+        const int row = hd.base_row + j * kBN;
+        {
+          const int s = j % C::kStagesK;
+          const uint32_t ph = (j / C::kStagesK) & 1;
+          mbar_wait(k_empty + s, ph ^ 1);
+          mbar_expect_tx(k_full + s, C::kTileBytes);
+          for (int b = 0; b < C::kBoxes; ++b)
+            tma_load_2d_hint(smem + C::kKOff + s * C::kTileBytes + b * C::kBoxBytes, kmap, k_full + s, b * 64,
+                             row, keep);
+        }
+        {
+          const int s = j % C::kStagesV;
+          const uint32_t ph = (j / C::kStagesV) & 1;
+          mbar_wait(v_empty + s, ph ^ 1);
+          mbar_expect_tx(v_full + s, C::kTileBytes);
+          for (int b = 0; b < C::kBoxes; ++b)
+            tma_load_2d_hint(smem + C::kVOff + s * C::kTileBytes + b * C::kBoxBytes, vmap, v_full + s, b * 64,
+                             row, keep);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = idesc_bf16(kBM, kBN, false);
+      constexpr uint32_t idesc_pv = idesc_bf16(kBM, D, true);
+      const uint32_t sQ = smem_u32(smem + C::kQOff);
+      const uint32_t sK = smem_u32(smem + C::kKOff);
+      const uint32_t sV = smem_u32(smem + C::kVOff);
+      const uint32_t tS0 = tmem, tS1 = tmem + 128;
+      const uint32_t tO0 = tmem + C::kTmemO, tO1 = tmem + C::kTmemO + D;
+
+      auto qk = [&](uint32_t d_tmem, int t, int ks) {
+        const uint32_t qa = sQ + t * C::kTileBytes;
+        const uint32_t kb = sK + ks * C::kTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * C::kBoxBytes + (kk & 3) * 32;
+          umma_ss(d_tmem, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(kb + off, 16, 1024), idesc_qk, kk > 0);
+        }
+      };
+      auto pv = [&](int t, int jj) {
+        const int vs = jj % C::kStagesV;
+        mbar_wait(p_full + t, jj & 1);
+        tc_fence_after();
+        if (t == 0) {
+          mbar_wait(v_full + vs, (jj / C::kStagesV) & 1);
+          tc_fence_after();
+        }
+        const uint32_t vb = sV + vs * C::kTileBytes;
+        const uint32_t tP = t ? tS1 : tS0;
+        const uint32_t tO = t ? tO1 : tO0;
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk)
+          umma_ts(tO, tP + kk * 8, sdesc_sw128(vb + kk * 2048, C::kBoxBytes, 1024), idesc_pv,
+                  (jj > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(o_full + t);
+        if (t == 1) umma_commit(v_empty + vs);
+      };
+
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      for (int j = 0; j < n_kv; ++j) {
+        const int ks = j % C::kStagesK;
+        mbar_wait(k_full + ks, (j / C::kStagesK) & 1);
+        tc_fence_after();
+        qk(tS0, 0, ks);
+        umma_commit(s_full + 0);
+        if (j > 0) pv(1, j - 1);
+        qk(tS1, 1, ks);
+        umma_commit(s_full + 1);
+        umma_commit(k_empty + ks);
+        pv(0, j);
+      }
+      pv(1, n_kv - 1);
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax
+    const int t = (warp - 4) >> 2;        // query tile of this warpgroup
+    const int quad = warp & 3;            // TMEM lane quadrant this warp may access
+    const int row_local = quad * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t tS = tmem + lane_off + t * 128;
+    const uint32_t tO = tmem + lane_off + C::kTmemO + t * D;
+    const float sl2 = p.scale_log2;
+    float m = -INFINITY;
+    float l = 0.f;
+    float reg_acc[3] = {0.f, 0.f, 0.f};  // probe: sink / neighbor / current mass
+
+    for (int j = 0; j < n_kv; ++j) {
+      mbar_wait(s_full + t, j & 1);
+      tc_fence_after();
+      uint32_t r[128];
+      tmem_ld32(tS + 0, r + 0);
+      tmem_ld32(tS + 32, r + 32);
+      tmem_ld32(tS + 64, r + 64);
+      tmem_ld32(tS + 96, r + 96);
+      tmem_wait_ld();
+      const int valid = hd.n_tok - j * kBN;
+      if (valid < kBN) {
+#pragma unroll
+        for (int c = 0; c < 128; ++c)
+          if (c >= valid) r[c] = __float_as_uint(-INFINITY);
+      }
+      float mx0 = __uint_as_float(r[0]), mx1 = __uint_as_float(r[1]);
+      float mx2 = __uint_as_float(r[2]), mx3 = __uint_as_float(r[3]);
+#pragma unroll
+      for (int c = 4; c < 128; c += 4) {
+        mx0 = fmaxf(mx0, __uint_as_float(r[c + 0]));
+        mx1 = fmaxf(mx1, __uint_as_float(r[c + 1]));
+        mx2 = fmaxf(mx2, __uint_as_float(r[c + 2]));
+        mx3 = fmaxf(mx3, __uint_as_float(r[c + 3]));
+      }
+      const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+      if (j == 0) {
+        m = m_tile;
+      } else {
+        const bool need = m_tile > m + kRescaleThreshold;
+        if (__any_sync(0xffffffffu, need)) {
+          const float alpha = need ? ex2(m - m_tile) : 1.f;
+          if (need) m = m_tile;
+          l *= alpha;
+          if constexpr (kProbe) {
+            reg_acc[0] *= alpha;
+            reg_acc[1] *= alpha;
+            reg_acc[2] *= alpha;
+          }
+          mbar_wait(o_full + t, (j - 1) & 1);  // O += P_{j-1} V_{j-1} has landed
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < D / 16; ++c) {
+            uint32_t o[16];
+            tmem_ld16(tO + c * 16, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st16(tO + c * 16, o);
+          }
+          tmem_wait_st();
+        }
+      }
+      const float neg_m = -m;
+      float sum0 = 0.f, sum1 = 0.f;
+      float span = 0.f;
+      int next_b = 0, kind = 0, slot = 0;
+      if constexpr (kProbe) {
+        const int c0 = j * kBN;
+        slot = min(c0 / p.hw, p.max_slots - 1);
+        next_b = (c0 / p.hw + 1) * p.hw - c0;
+        kind = p.region_tab[h * p.max_slots + slot];
+      }
+#pragma unroll
+      for (int quarter = 0; quarter < 4; ++quarter) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int c = quarter * 32 + 2 * i;
+          const float a = ex2(fmaf(__uint_as_float(r[c]), sl2, neg_m));
+          const float b = ex2(fmaf(__uint_as_float(r[c + 1]), sl2, neg_m));
+          sum0 += a;
+          sum1 += b;
+          pk[i] = pack_bf16x2(a, b);
+          if constexpr (kProbe) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              if (c + e == next_b) {  // warp-uniform region boundary
+                reg_acc[0] += kind == 0 ? span : 0.f;
+                reg_acc[1] += kind == 1 ? span : 0.f;
+                reg_acc[2] += kind == 2 ? span : 0.f;
+                span = 0.f;
+                next_b += p.hw;
+                slot = min(slot + 1, p.max_slots - 1);
+                kind = p.region_tab[h * p.max_slots + slot];
+              }
+              span += e ? b : a;
+            }
+          }
+        }
+        tmem_st16(tS + quarter * 16, pk);
+      }
+      if constexpr (kProbe) {
+        reg_acc[0] += kind == 0 ? span : 0.f;
+        reg_acc[1] += kind == 1 ? span : 0.f;
+        reg_acc[2] += kind == 2 ? span : 0.f;
+      }
+      l += sum0 + sum1;
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_full + t);
+    }
+
+    // ------------------------------------------------------------ epilogue
+    mbar_wait(o_full + t, (n_kv - 1) & 1);
+    tc_fence_after();
+    const int row = qp * 2 * kBM + t * kBM + row_local;
+    const bool row_ok = row < p.hw;
+    const float inv_l = 1.f / l;
+    __nv_bfloat16* orow = p.out + (static_cast<int64_t>(hd.o_head) * p.hw + row) * p.out_ld;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t o[32];
+      tmem_ld32(tO + c * 32, o);
+      tmem_wait_ld();
+      if (row_ok) {
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int col = c * 32 + v * 8;
+          if (col < p.d_out) {
+            uint4 w;
+            w.x = pack_bf16x2(__uint_as_float(o[v * 8 + 0]) * inv_l, __uint_as_float(o[v * 8 + 1]) * inv_l);
+            w.y = pack_bf16x2(__uint_as_float(o[v * 8 + 2]) * inv_l, __uint_as_float(o[v * 8 + 3]) * inv_l);
+            w.z = pack_bf16x2(__uint_as_float(o[v * 8 + 4]) * inv_l, __uint_as_float(o[v * 8 + 5]) * inv_l);
+            w.w = pack_bf16x2(__uint_as_float(o[v * 8 + 6]) * inv_l, __uint_as_float(o[v * 8 + 7]) * inv_l);
+            *reinterpret_cast<uint4*>(orow + col) = w;
+          }
+        }
+      }
+    }
+    if constexpr (kProbe) {
+      if (row_ok && p.row_sampled[row]) {
+        float* dst = p.probe_rows + (static_cast<int64_t>(h) * p.hw + row) * 3;
+        dst[0] = reg_acc[0] * inv_l;
+        dst[1] = reg_acc[1] * inv_l;
+        dst[2] = reg_acc[2] * inv_l;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int D, bool kProbe>
+static int launch_attn(const AttnParams& p, int grid, cudaStream_t stream) {
+  using C = AttnCfg<D>;
+  auto kern = df_attn_kernel<D, kProbe>;
+  static bool configured = false;  // benign race: idempotent attribute set
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(df_attn_kernel)", e);
+    configured = true;
+  }
+  kern<<<grid, kThreads, C::kSmem, stream>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error("df_attn_kernel launch", e);
+  return DF_OK;
+}
+
+}  // namespace dfb
+
+using namespace dfb;
+
+extern "C" int df_attn_fwd(const df_attn_args* a, void* stream) {
+  if (!a) return set_error(DF_E_ARG, "df_attn_fwd: null args");
+  if (a->head_dim != 64 && a->head_dim != 128)
+    return set_error(DF_E_SHAPE, "df_attn_fwd: head_dim must be 64 or 128 (got %d)", a->head_dim);
+  if (a->d_out < 8 || a->d_out > a->head_dim || (a->d_out % 8) != 0)
+    return set_error(DF_E_SHAPE, "df_attn_fwd: d_out %d must be a multiple of 8 in [8, head_dim]", a->d_out);
+  if (a->num_heads < 1 || a->num_heads > DF_MAX_HEADS)
+    return set_error(DF_E_SHAPE, "df_attn_fwd: num_heads %d outside [1, %d]", a->num_heads, DF_MAX_HEADS);
+  if (a->num_arenas < 1 || a->num_arenas > DF_MAX_ARENAS)
+    return set_error(DF_E_ARG, "df_attn_fwd: num_arenas %d outside [1, %d]", a->num_arenas, DF_MAX_ARENAS);
+  if (a->hw < 1) return set_error(DF_E_SHAPE, "df_attn_fwd: hw must be >= 1");
+  if (!a->q || !a->out || !a->heads || !a->kv_maps) return set_error(DF_E_ARG, "df_attn_fwd: null pointer");
+  if (a->out_ld < a->d_out) return set_error(DF_E_SHAPE, "df_attn_fwd: out_ld < d_out");
+  if (a->q_rows < 1 || a->q_rows > INT32_MAX) return set_error(DF_E_SHAPE, "df_attn_fwd: bad q_rows");
+  if ((reinterpret_cast<uintptr_t>(a->q) & 15) || (reinterpret_cast<uintptr_t>(a->out) & 15) || (a->out_ld % 8))
+    return set_error(DF_E_ARG, "df_attn_fwd: q/out must be 16-byte aligned, out_ld a multiple of 8");
+  const bool probe = (a->flags & DF_ATTN_PROBE) != 0;
+  if (probe && (!a->region_of_slot || !a->row_sampled || !a->probe_rows || a->max_slots < 1))
+    return set_error(DF_E_ARG, "df_attn_fwd: probe epilogue needs region_of_slot, row_sampled, probe_rows");
+
+  AttnParams p;
+  std::memset(&p, 0, sizeof(p));
+  int rc = encode_rowmajor_bf16(&p.qmap, a->q, a->q_rows, a->head_dim);
+  if (rc != DF_OK) return rc;
+  std::memcpy(p.kvmap, a->kv_maps, static_cast<size_t>(a->num_arenas) * 2 * DF_TMAP_BYTES);
+  p.out = static_cast<__nv_bfloat16*>(a->out);
+  p.out_ld = a->out_ld;
+  p.hw = a->hw;
+  p.d_out = a->d_out;
+  p.n_heads = a->num_heads;
+  p.n_qpairs = (a->hw + 2 * kBM - 1) / (2 * kBM);
+  p.max_slots = probe ? a->max_slots : 1;
+  p.region_tab = a->region_of_slot;
+  p.row_sampled = a->row_sampled;
+  p.probe_rows = a->probe_rows;
+  p.scale_log2 = a->scale * 1.4426950408889634f;
+
+  int order[DF_MAX_HEADS];
+  for (int i = 0; i < a->num_heads; ++i) {
+    const df_head_desc& h = a->heads[i];
+    if (h.n_tok < 1) return set_error(DF_E_SHAPE, "df_attn_fwd: head %d has empty context", i);
+    if (h.arena < 0 || h.arena >= a->num_arenas) return set_error(DF_E_ARG, "df_attn_fwd: head %d bad arena", i);
+    if (h.base_row < 0 || h.base_row + h.n_tok > INT32_MAX)
+      return set_error(DF_E_ARG, "df_attn_fwd: head %d arena rows out of int32 range", i);
+    if (h.q_head < 0 || static_cast<int64_t>(h.q_head) * a->hw >= a->q_rows || h.o_head < 0 || h.q_head > 32767 ||
+        h.o_head > 32767)
+      return set_error(DF_E_SHAPE, "df_attn_fwd: head %d q/o index out of range", i);
+    p.heads[i].base_row = static_cast<int32_t>(h.base_row);
+    p.heads[i].n_tok = h.n_tok;
+    p.heads[i].q_head = static_cast<int16_t>(h.q_head);
+    p.heads[i].o_head = static_cast<int16_t>(h.o_head);
+    p.heads[i].arena = static_cast<int16_t>(h.arena);
+    order[i] = i;
+  }
+  // Longest context first: the block scheduler then issues the heaviest work
+  // items first (LPT), keeping the tail short when heads are heterogeneous.
+  std::stable_sort(order, order + a->num_heads,
+                   [&](int x, int y) { return a->heads[x].n_tok > a->heads[y].n_tok; });
+  for (int i = 0; i < a->num_heads; ++i) p.head_order[i] = static_cast<uint8_t>(order[i]);
+
+  const int grid = a->num_heads * p.n_qpairs;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (a->head_dim == 128)
+    return probe ? launch_attn<128, true>(p, grid, s) : launch_attn<128, false>(p, grid, s);
+  return probe ? launch_attn<64, true>(p, grid, s) : launch_attn<64, false>(p, grid, s);
+}

@@ -1,0 +1,20 @@
+// df_internal.h -- shared host-side helpers of libdfb200 (not part of the ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "df_b200.h"
+
+namespace dfb {
+
+// Record a thread-local error message (printf-style) and return `code`.
+int set_error(int code, const char* fmt, ...);
+int set_cuda_error(const char* what, cudaError_t e);
+
+// TMA descriptor for a row-major bf16 matrix [rows][width] (width 64 or 128),
+// box = 128 rows x 64 columns (128 bytes), SWIZZLE_128B, OOB -> zero.
+int encode_rowmajor_bf16(CUtensorMap* map, const void* base, int64_t rows, int32_t width);
+
+}  // namespace dfb

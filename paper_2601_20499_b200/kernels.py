@@ -1,0 +1,234 @@
+"""Torch-facing wrappers of the C ABI: KV arenas and the three device ops.
+
+Only device tensors cross into the library (as raw pointers).  Nothing here
+computes on the CPU: a missing extension or device raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .errors import ShapeError
+
+TOKEN_ALIGN = 128  # head regions start on a kv-tile boundary
+SUPPORTED_WIDTHS = (64, 128)
+
+
+def padded_width(head_dim: int) -> int:
+    """Arena / Q row width the kernel runs at for a given head_dim."""
+    if head_dim < 1 or head_dim > 128:
+        raise ShapeError(f"head_dim {head_dim} outside [1, 128] on the B200 path")
+    return 64 if head_dim <= 64 else 128
+
+
+def _stream_handle(stream: torch.cuda.Stream | None) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class KVArena:
+    """One device allocation holding the K and V rings of many heads.
+
+    Layout: two bf16 planes ``k``/``v`` of shape [rows, width]; each head owns
+    a region of whole frames starting on a 128-token boundary (so a head's
+    last kv tile never straddles into another head's region except through
+    zero/stale rows that the kernel masks).  The TMA descriptors of both
+    planes are encoded once here and passed by value to every launch.
+    """
+
+    def __init__(self, total_rows: int, width: int, device: torch.device | str):
+        if width not in SUPPORTED_WIDTHS:
+            raise ShapeError(f"arena width {width} not in {SUPPORTED_WIDTHS}")
+        total_rows = max(int(total_rows), TOKEN_ALIGN)
+        self.device = torch.device(device)
+        self.width = width
+        self.rows = total_rows
+        # zero-init: rows past a head's context are read (then masked) by the
+        # last partial kv tile; zeros keep them finite.
+        self.k = torch.zeros(total_rows, width, dtype=torch.bfloat16, device=self.device)
+        self.v = torch.zeros(total_rows, width, dtype=torch.bfloat16, device=self.device)
+        _lib.require_device(self.device.index if self.device.index is not None else torch.cuda.current_device())
+        buf = (ctypes.c_uint8 * (2 * _lib.DF_TMAP_BYTES))()
+        _lib.call(
+            "df_kv_arena_maps",
+            ctypes.c_void_p(self.k.data_ptr()),
+            ctypes.c_void_p(self.v.data_ptr()),
+            ctypes.c_int64(total_rows),
+            ctypes.c_int32(width),
+            buf,
+        )
+        self.maps = bytes(buf)
+        self._next = 0
+
+    def allocate(self, tokens: int) -> int:
+        """Reserve a region of ``tokens`` rows; returns its first row."""
+        start = self._next
+        need = int(math.ceil(max(tokens, 1) / TOKEN_ALIGN) * TOKEN_ALIGN)
+        if start + need > self.rows:
+            raise ShapeError(f"arena full: {start}+{need} > {self.rows} rows")
+        self._next = start + need
+        return start
+
+    @staticmethod
+    def region_rows(tokens: int) -> int:
+        return int(math.ceil(max(tokens, 1) / TOKEN_ALIGN) * TOKEN_ALIGN)
+
+    @property
+    def nbytes(self) -> int:
+        return 2 * self.rows * self.width * 2
+
+
+@dataclass
+class HeadWork:
+    """One head of one attention launch (df_head_desc)."""
+
+    arena: KVArena
+    base_row: int
+    n_tok: int
+    q_head: int
+    o_head: int
+
+
+@dataclass
+class ProbeBuffers:
+    """Device buffers of the fused DHP epilogue for one launch."""
+
+    region_of_slot: torch.Tensor  # uint8 [heads, max_slots]
+    row_sampled: torch.Tensor  # uint8 [hw]
+    probe_rows: torch.Tensor  # float32 [heads, hw, 3]
+
+
+def attention(
+    q: torch.Tensor,
+    out: torch.Tensor,
+    work: list[HeadWork],
+    hw: int,
+    scale: float,
+    probe: ProbeBuffers | None = None,
+    stream: torch.cuda.Stream | None = None,
+) -> None:
+    """One ragged launch over every head in ``work``.
+
+    ``q``: bf16 [q_heads*hw, width] (width = arena width); ``out``: bf16
+    [o_heads*hw, d_out] with row stride ``out.stride(0)``.
+    """
+    if not work:
+        return
+    if len(work) > _lib.DF_MAX_HEADS:
+        # more heads than one launch carries: split (still one stream, in order)
+        for i in range(0, len(work), _lib.DF_MAX_HEADS):
+            sub_probe = None
+            if probe is not None:
+                sl = slice(i, i + _lib.DF_MAX_HEADS)
+                sub_probe = ProbeBuffers(probe.region_of_slot[sl], probe.row_sampled, probe.probe_rows[sl])
+            attention(q, out, work[i : i + _lib.DF_MAX_HEADS], hw, scale, sub_probe, stream)
+        return
+    if q.dtype != torch.bfloat16 or out.dtype != torch.bfloat16:
+        raise ShapeError("q and out must be bfloat16")
+    if not q.is_cuda or not out.is_cuda:
+        raise ShapeError("q and out must be CUDA tensors")
+    width = work[0].arena.width
+    if q.dim() != 2 or q.shape[1] != width or not q.is_contiguous():
+        raise ShapeError(f"q must be contiguous [rows, {width}], got {tuple(q.shape)}")
+    if out.dim() != 2 or out.stride(1) != 1:
+        raise ShapeError("out must be a row-major 2-D view")
+    arenas: list[KVArena] = []
+    idx: dict[int, int] = {}
+    descs = (_lib.HeadDesc * len(work))()
+    for i, w in enumerate(work):
+        if w.arena.width != width:
+            raise ShapeError("all heads of one launch must share the arena width")
+        a = idx.get(id(w.arena))
+        if a is None:
+            a = len(arenas)
+            if a >= _lib.DF_MAX_ARENAS:
+                raise ShapeError(f"more than {_lib.DF_MAX_ARENAS} KV arenas in one layer")
+            idx[id(w.arena)] = a
+            arenas.append(w.arena)
+        descs[i].base_row = w.base_row
+        descs[i].n_tok = w.n_tok
+        descs[i].q_head = w.q_head
+        descs[i].o_head = w.o_head
+        descs[i].arena = a
+    maps = b"".join(a.maps for a in arenas)
+    maps_buf = ctypes.create_string_buffer(maps, len(maps))
+    args = _lib.AttnArgs()
+    args.q = q.data_ptr()
+    args.q_rows = q.shape[0]
+    args.out = out.data_ptr()
+    args.out_ld = out.stride(0)
+    args.hw = hw
+    args.head_dim = width
+    args.d_out = out.shape[1]
+    args.scale = scale
+    args.num_heads = len(work)
+    args.num_arenas = len(arenas)
+    args.heads = descs
+    args.kv_maps = ctypes.cast(maps_buf, ctypes.c_void_p)
+    if probe is not None:
+        args.flags = _lib.DF_ATTN_PROBE
+        args.max_slots = probe.region_of_slot.shape[1]
+        args.region_of_slot = probe.region_of_slot.data_ptr()
+        args.row_sampled = probe.row_sampled.data_ptr()
+        args.probe_rows = probe.probe_rows.data_ptr()
+    _lib.call("df_attn_fwd", ctypes.byref(args), _stream_handle(stream))
+
+
+def copy_segments(segs: list[tuple[int, int, int, int, int, int]], stream: torch.cuda.Stream | None = None) -> None:
+    """Batched 16-byte-vectorised device copies, (src, dst, rows, src_ld, dst_ld, row_bytes) each."""
+    for i in range(0, len(segs), _lib.DF_MAX_APPEND_SEGS):
+        chunk = segs[i : i + _lib.DF_MAX_APPEND_SEGS]
+        arr = (_lib.CopySeg * len(chunk))()
+        for j, s in enumerate(chunk):
+            arr[j].src, arr[j].dst, arr[j].rows, arr[j].src_ld, arr[j].dst_ld, arr[j].row_bytes = s
+        _lib.call("df_kv_append", arr, ctypes.c_int32(len(chunk)), _stream_handle(stream))
+
+
+class PackPlan:
+    """A device-resident segment list for df_kv_pack (built once, launched once)."""
+
+    def __init__(self, segs: list[tuple[int, int, int, int, int, int]], device: torch.device):
+        n = len(segs)
+        arr = (_lib.CopySeg * max(n, 1))()
+        for j, s in enumerate(segs):
+            arr[j].src, arr[j].dst, arr[j].rows, arr[j].src_ld, arr[j].dst_ld, arr[j].row_bytes = s
+        prefix = (ctypes.c_int64 * (n + 1))()
+        total = ctypes.c_int64(0)
+        _lib.call("df_kv_pack_plan", arr, ctypes.c_int32(n), prefix, ctypes.byref(total))
+        self.n = n
+        self.total_blocks = int(total.value)
+        self.bytes_moved = sum(2 * s[2] * s[5] for s in segs)  # read + write
+        raw = bytes(memoryview(arr).cast("B"))[: n * ctypes.sizeof(_lib.CopySeg)]
+        self.segs_dev = torch.frombuffer(bytearray(raw) or bytearray(8), dtype=torch.uint8).to(device)
+        self.prefix_dev = torch.tensor(list(prefix), dtype=torch.int64, device=device)
+
+    def launch(self, stream: torch.cuda.Stream | None = None) -> None:
+        _lib.call(
+            "df_kv_pack",
+            ctypes.c_void_p(self.segs_dev.data_ptr()),
+            ctypes.c_void_p(self.prefix_dev.data_ptr()),
+            ctypes.c_int32(self.n),
+            ctypes.c_int64(self.total_blocks),
+            _stream_handle(stream),
+        )
+
+
+def scores_finalize(probe: ProbeBuffers, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Per-head mean region masses over the sampled rows -> float64 [heads, 3]."""
+    heads, hw = probe.probe_rows.shape[0], probe.probe_rows.shape[1]
+    F = torch.empty(heads, 3, dtype=torch.float64, device=probe.probe_rows.device)
+    _lib.call(
+        "df_scores_finalize",
+        ctypes.c_void_p(probe.probe_rows.data_ptr()),
+        ctypes.c_void_p(probe.row_sampled.data_ptr()),
+        ctypes.c_int32(heads),
+        ctypes.c_int32(hw),
+        ctypes.c_void_p(F.data_ptr()),
+        _stream_handle(stream),
+    )
+    return F
