@@ -1,0 +1,475 @@
+"""numpy (fp64) restatement of the reference Dummy Forcing hot path.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Citations are to
+/root/reference/pkg/src/dummy_forcing/<file>:<line>.  Parity pinned by
+tests/test_oracle_golden.py against vectors produced by the reference.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+SINK, NEIGHBOR, DUMMY = 0, 1, 2  # head_programming.py:254 code order
+CLASS_NAMES = ("sink", "neighbor", "dummy")
+
+# --------------------------------------------------------------------- rng
+# rng.py:27-65: splitmix64 in counter mode.
+_G = np.uint64(0x9E3779B97F4A7C15)
+_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_M2 = np.uint64(0x94D049BB133111EB)
+
+
+def mix64(x):
+    """rng.py:27-34."""
+    z = np.asarray(x, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = (z ^ (z >> np.uint64(30))) * _M1
+        z = (z ^ (z >> np.uint64(27))) * _M2
+        z = z ^ (z >> np.uint64(31))
+    return z if z.ndim else np.uint64(z)
+
+
+def derive(seed: int, label: str, *indices: int) -> int:
+    """rng.py:37-45: fold label bytes then indices through mix64."""
+    h = np.uint64(seed & 0xFFFFFFFFFFFFFFFF)
+    with np.errstate(over="ignore"):
+        for b in label.encode("utf-8"):
+            h = mix64(h ^ np.uint64(b))
+        for i in indices:
+            h = mix64(h ^ np.uint64(i & 0xFFFFFFFFFFFFFFFF))
+    return int(h)
+
+
+def uniform(seed: int, n: int, offset: int = 0) -> np.ndarray:
+    """rng.py:48-54: top 53 bits of mix64(seed + (i+1)*gamma)."""
+    ctr = np.arange(offset + 1, offset + n + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        st = np.uint64(seed & 0xFFFFFFFFFFFFFFFF) + ctr * _G
+    return (mix64(st) >> np.uint64(11)).astype(np.float64) * (2.0**-53)
+
+
+def symmetric(seed: int, shape, offset: int = 0) -> np.ndarray:
+    """rng.py:57-60."""
+    n = int(np.prod(shape)) if shape else 1
+    return (uniform(seed, n, offset) * 2.0 - 1.0).reshape(shape)
+
+
+def matrix(seed: int, rows: int, cols: int, scale: float = 1.0) -> np.ndarray:
+    """rng.py:63-65."""
+    return symmetric(seed, (rows, cols)) * scale
+
+
+# ------------------------------------------------------------------ config
+@dataclass(frozen=True)
+class Config:
+    """Fields and defaults of SessionConfig (config.py:10-59)."""
+
+    num_layers: int
+    num_heads: int
+    head_dim: int
+    HW: int
+    window_len: int
+    ar_steps: int
+    denoise_steps: int = 1
+    sink_frame: int = 0
+    dummy_count: int = 0
+    packing_enabled: bool = True
+    probe_ar_step: int = 2
+    probe_denoise_step: int | None = None
+    subsample_ratio: float = 1.0
+    merged_window: int | None = None
+    context_extension: bool = False
+
+    @property
+    def total_heads(self) -> int:
+        return self.num_layers * self.num_heads
+
+
+# ---------------------------------------------------------------- policies
+@dataclass(frozen=True)
+class Policy:
+    """kv_cache.py:58-101."""
+
+    kind: str
+    window_len: int
+    sink_frame: int = 0
+    extended_window: int | None = None
+
+    @property
+    def recent_capacity(self) -> int:
+        return {
+            "baseline_window": self.window_len - 1,
+            "sink_only": 0,
+            "neighbor_window": self.extended_window if self.extended_window is not None else self.window_len - 1,
+            "dummy_empty": 0,
+            "dummy_packed": 1,
+        }[self.kind]
+
+    @property
+    def keeps_sink(self) -> bool:
+        return self.kind in ("baseline_window", "sink_only")
+
+    def warm_past_frames(self) -> int:
+        return self.recent_capacity + int(self.keeps_sink)
+
+
+def baseline_policy(cfg: Config) -> Policy:
+    """kv_cache.py:135-140."""
+    return Policy("baseline_window", cfg.window_len, cfg.sink_frame)
+
+
+def derive_policy(cls: int, cfg: Config, ext: int | None = None) -> Policy:
+    """kv_cache.py:104-132."""
+    if cls == DUMMY:
+        return Policy("dummy_packed" if cfg.packing_enabled else "dummy_empty", cfg.window_len, cfg.sink_frame)
+    if cfg.merged_window is not None:
+        return Policy("baseline_window", cfg.merged_window, cfg.sink_frame)
+    if cls == SINK:
+        return Policy("sink_only", cfg.window_len, cfg.sink_frame)
+    if cfg.context_extension and ext is not None:
+        return Policy("neighbor_window", cfg.window_len, cfg.sink_frame, ext)
+    return Policy("neighbor_window", cfg.window_len, cfg.sink_frame)
+
+
+def extension_window(classes, cfg: Config) -> int | None:
+    """kv_cache.py:143-158: floor-split of the freed budget over neighbor heads."""
+    classes = list(classes)
+    n_nb = classes.count(NEIGHBOR)
+    if n_nb == 0:
+        return None
+    used = classes.count(SINK) + classes.count(DUMMY) * (1 if cfg.packing_enabled else 0)
+    return max((len(classes) * cfg.window_len - used) // n_nb, cfg.window_len - 1)
+
+
+def evict(frame_ids: list[int], p: Policy) -> list[int]:
+    """kv_cache.py:187-197: pinned sink + the newest recent_capacity others."""
+    sink = [f for f in frame_ids if p.keeps_sink and f == p.sink_frame]
+    rest = [f for f in frame_ids if not (p.keeps_sink and f == p.sink_frame)]
+    keep = min(p.recent_capacity, len(rest))
+    return sorted(sink + (rest[len(rest) - keep :] if keep else []))
+
+
+def append(frame_ids: list[int], fid: int, p: Policy) -> list[int]:
+    """kv_cache.py:177-185 (OrderingError on a stale id)."""
+    if frame_ids and fid <= frame_ids[-1]:
+        raise ValueError(f"frame {fid} not newer than {frame_ids[-1]}")
+    return evict(frame_ids + [fid], p)
+
+
+def rebuild(frame_ids: list[int], p: Policy) -> list[int]:
+    """kv_cache.py:199-201: re-append the history under the new policy."""
+    out: list[int] = []
+    for f in frame_ids:
+        out = append(out, f, p)
+    return out
+
+
+def region_kinds(frame_ids: list[int], p: Policy) -> list[str]:
+    """kv_cache.py:214-217: per context frame (cached + current) labels."""
+    return ["sink" if f == p.sink_frame else "neighbor" for f in frame_ids] + ["current"]
+
+
+def cache_reduction_ratio(classes, cfg: Config) -> float:
+    """kv_cache.py:239-260."""
+    ext = extension_window(classes, cfg) if cfg.context_extension else None
+    per = [derive_policy(c, cfg, ext).warm_past_frames() for c in classes]
+    return sum(per) / (len(per) * cfg.window_len)
+
+
+# --------------------------------------------------------------- attention
+def batched_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, scale: float) -> np.ndarray:
+    """engine.py:87-98: max-subtracted softmax(q k^T * scale) v per batch."""
+    s = np.matmul(q, np.swapaxes(k, 1, 2)) * scale
+    s = np.exp(s - s.max(axis=-1, keepdims=True))
+    return np.matmul(s / s.sum(axis=-1, keepdims=True), v)
+
+
+def mode_groups(classes: list[int] | None, mode: str, num_heads: int) -> list[list[int]]:
+    """engine.py:150-158,192-195: head groups of one layer, in call order."""
+    if mode == "baseline" or classes is None:
+        return [list(range(num_heads))]
+    if mode == "hma":
+        return [[h for h, c in enumerate(classes) if c == want] for want in (DUMMY, SINK, NEIGHBOR)]
+    if mode == "packed":
+        ds = [h for h, c in enumerate(classes) if c != NEIGHBOR]
+        nb = [h for h, c in enumerate(classes) if c == NEIGHBOR]
+        return [ds, nb]
+    raise ValueError(mode)
+
+
+def run_groups(q_heads: np.ndarray, ctx_k: list[np.ndarray], ctx_v: list[np.ndarray], groups, head_dim: int):
+    """engine.py:111-137: returns (outputs, kernel_calls, key_token_macs)."""
+    out = np.empty_like(q_heads)
+    scale = 1.0 / math.sqrt(head_dim)
+    calls = macs = 0
+    for g in groups:
+        if not g:
+            continue
+        lens = {ctx_k[h].shape[0] for h in g}
+        if len(lens) != 1:
+            raise ValueError(f"context lengths {sorted(lens)} differ within one batch")
+        k = np.stack([ctx_k[h] for h in g])
+        v = np.stack([ctx_v[h] for h in g])
+        out[g] = batched_attention(q_heads[g], k, v, scale)
+        calls += 1
+        macs += len(g) * q_heads.shape[1] * k.shape[1] * head_dim
+    return out, calls, macs
+
+
+def past_frames(p: Policy, history: int) -> int:
+    """engine.py:217-227."""
+    if history == 0:
+        return 0
+    sink_seen = p.sink_frame < history
+    if p.kind == "baseline_window":
+        non_sink = history - 1 if sink_seen else history
+        return min(non_sink, p.window_len - 1) + int(sink_seen)
+    if p.kind == "sink_only":
+        return int(sink_seen)
+    return min(history, p.recent_capacity)
+
+
+def expected_step_macs(cfg: Config, mode: str, history: int, classes=None) -> int:
+    """engine.py:198-237: closed-form QK^T MACs of one denoise iteration."""
+    ext = extension_window(classes, cfg) if (classes is not None and cfg.context_extension) else None
+    if mode == "baseline" or classes is None:
+        ctxs = [(past_frames(baseline_policy(cfg), history) + 1) * cfg.HW] * cfg.total_heads
+    else:
+        ctxs = [(past_frames(derive_policy(c, cfg, ext), history) + 1) * cfg.HW for c in classes]
+    return sum(cfg.HW * c * cfg.head_dim for c in ctxs)
+
+
+# ---------------------------------------------------------------- profiler
+def subsample_rows(n: int, ratio: float) -> np.ndarray:
+    """profiler.py:132-144."""
+    c = int(n * ratio)
+    if c < 1:
+        raise ValueError("no rows")
+    return (np.arange(c, dtype=np.int64) * n) // c
+
+
+def region_scores(attn: np.ndarray, kinds: list[str], hw: int) -> np.ndarray:
+    """profiler.py:105-129: region mass summed over rows / rows."""
+    acc = {"sink": 0.0, "neighbor": 0.0, "current": 0.0}
+    for i, kd in enumerate(kinds):
+        acc[kd] += float(attn[:, i * hw : (i + 1) * hw].sum())
+    inv = 1.0 / attn.shape[0]
+    return np.array([acc["sink"] * inv, acc["neighbor"] * inv, acc["current"] * inv])
+
+
+def probe_scores(q: np.ndarray, keys: np.ndarray, kinds: list[str], hw: int, ratio: float, head_dim: int):
+    """profiler.py:160-167 for one head."""
+    rows = subsample_rows(q.shape[0], ratio)
+    s = (q[rows] @ keys.T) * (1.0 / np.sqrt(head_dim))
+    s = np.exp(s - s.max(axis=1, keepdims=True))
+    s = s / s.sum(axis=1, keepdims=True)
+    return region_scores(s, kinds, hw)
+
+
+# ------------------------------------------------------------- classifier
+def greedy_classify(F: np.ndarray, n_dummy: int):
+    """head_programming.py:141-164: (codes, objective)."""
+    F = np.asarray(F, dtype=np.float64)
+    total = F.shape[0]
+    if not 0 <= n_dummy <= total:
+        raise ValueError("n_dummy out of range")
+    cost = np.maximum(F[:, 0], F[:, 1])
+    order = np.lexsort((np.arange(total), cost))
+    codes = np.where(F[:, 0] >= F[:, 1], SINK, NEIGHBOR)
+    codes[order[:n_dummy]] = DUMMY
+    table = np.stack([F[:, 0] + F[:, 2], F[:, 1] + F[:, 2], F[:, 2]], axis=1)
+    return codes.astype(np.int64), float(np.sum(table[np.arange(total), codes]))
+
+
+# ----------------------------------------------------------- planted model
+class PlantedStream:
+    """scenario.py:167-275: open-loop Q/K/V with region-biased logits."""
+
+    def __init__(self, labels, margin: float, noise_seed: int, cfg: Config, row_noise: float = 0.05):
+        self.labels = tuple(labels)
+        self.margin = margin
+        self.noise_seed = noise_seed
+        self.cfg = cfg
+        self.row_noise = row_noise
+        self._dirs: dict[int, np.ndarray] = {}
+
+    def _dir(self, f: int) -> np.ndarray:
+        d = self._dirs.get(f)
+        if d is None:
+            v = symmetric(derive(self.noise_seed, "dir", f), (self.cfg.head_dim,))
+            d = self._dirs[f] = v / np.linalg.norm(v)
+        return d
+
+    def _window(self, i: int) -> list[int]:
+        c = self.cfg
+        fr = set(range(max(i - (c.window_len - 1), 0), i + 1))
+        if c.sink_frame < i:
+            fr.add(c.sink_frame)
+        return sorted(fr)
+
+    def _targets(self, label: str, i: int) -> list[int]:
+        c = self.cfg
+        if label == "current":
+            return [i]
+        if label == "sink":
+            return [c.sink_frame] if c.sink_frame < i else [i]
+        fr = [f for f in range(max(i - (c.window_len - 1), 0), i) if f != c.sink_frame]
+        return fr or [i]
+
+    def frame_input(self, i: int, t: int):
+        return None
+
+    def qkv(self, layer: int, x, i: int, t: int):
+        c = self.cfg
+        q = np.empty((c.num_heads, c.HW, c.head_dim))
+        k = np.empty_like(q)
+        v = np.empty_like(q)
+        win = self._window(i)
+        for h in range(c.num_heads):
+            flat = layer * c.num_heads + h
+            tgt = set(self._targets(self.labels[flat], i))
+            base = np.zeros(c.head_dim)
+            for f in win:
+                base = base + (self.margin if f in tgt else 0.0) * self._dir(f)
+            q[h] = math.sqrt(c.head_dim) * base[None, :] + self.row_noise * matrix(
+                derive(self.noise_seed, "q", layer, h, i, t), c.HW, c.head_dim
+            )
+            k[h] = self._dir(i)[None, :] + self.row_noise * matrix(derive(self.noise_seed, "k", layer, h, i), c.HW, c.head_dim)
+            v[h] = matrix(derive(self.noise_seed, "v", layer, h, i), c.HW, c.head_dim)
+        return q, k, v
+
+    def mix(self, layer: int, outputs):
+        return None
+
+
+def planted_setup(seed: int, margin: float, num_layers=2, num_heads=8, subsample_ratio=1.0, **over):
+    """tests/conftest.py:29-59 of the reference (4 sink, 6 neighbor, 6 current)."""
+    cfg = Config(
+        num_layers=num_layers, num_heads=num_heads, head_dim=32, HW=8, window_len=4, ar_steps=4,
+        denoise_steps=2, dummy_count=6, probe_ar_step=2, subsample_ratio=subsample_ratio,
+    )
+    cfg = replace(cfg, **over)
+    labels = ("sink",) * 4 + ("neighbor",) * 6 + ("current",) * 6
+    order = np.random.default_rng(seed).permutation(len(labels))
+    labels = tuple(labels[i] for i in order)
+    return cfg, labels, derive(seed, "planted")
+
+
+# ---------------------------------------------------------------- session
+@dataclass
+class LayerTrace:
+    ar_step: int
+    denoise_step: int
+    layer: int
+    q: np.ndarray
+    k: np.ndarray
+    v: np.ndarray
+    outputs: np.ndarray
+    context_frames: list[list[int]]
+    kernel_calls: int
+    macs: int
+
+
+@dataclass
+class OracleRun:
+    classes: list[int] | None = None
+    objective: float | None = None
+    F: np.ndarray | None = None
+    frame_ids_after_step: list[list[list[int]]] = field(default_factory=list)
+    kernel_calls_steady: list[int] = field(default_factory=list)
+    step_macs: list[int] = field(default_factory=list)
+    cache_ratio: float = 1.0
+    traces: list[LayerTrace] = field(default_factory=list)
+
+
+def run_session(model, cfg: Config, mode: str, keep_traces: bool = False, qkv_hook=None) -> OracleRun:
+    """engine.py:268-476 at frame-id + fp64 numerics level (open-loop models).
+
+    ``qkv_hook(layer, ar, t, q, k, v)`` may replace the model's Q/K/V (used to
+    feed the oracle the same bf16-rounded inputs as the device).
+    """
+    run = OracleRun()
+    L, H, hw = cfg.num_layers, cfg.num_heads, cfg.HW
+    base = baseline_policy(cfg)
+    pol = [[base] * H for _ in range(L)]
+    ids: list[list[list[int]]] = [[[] for _ in range(H)] for _ in range(L)]
+    data: dict[tuple[int, int, int], tuple[np.ndarray, np.ndarray]] = {}
+    classify_at = None
+    if mode != "baseline" and cfg.dummy_count > 0 and cfg.probe_ar_step < cfg.ar_steps:
+        dn = cfg.probe_denoise_step if cfg.probe_denoise_step is not None else cfg.denoise_steps - 1
+        classify_at = (cfg.probe_ar_step, dn)
+    captured = []
+    for i in range(cfg.ar_steps):
+        eff = "baseline" if run.classes is None else mode
+        final_kv = []
+        macs = 0
+        calls = []
+        for t in range(cfg.denoise_steps):
+            x = model.frame_input(i, t)
+            for layer in range(L):
+                q, k, v = model.qkv(layer, x, i, t)
+                if qkv_hook is not None:
+                    q, k, v = qkv_hook(layer, i, t, q, k, v)
+                ck, cv, frames = [], [], []
+                for h in range(H):
+                    fl = ids[layer][h] + [i]
+                    ck.append(np.concatenate([data[(layer, h, f)][0] for f in ids[layer][h]] + [k[h]]))
+                    cv.append(np.concatenate([data[(layer, h, f)][1] for f in ids[layer][h]] + [v[h]]))
+                    frames.append(fl)
+                cls_l = None if run.classes is None else run.classes[layer * H : (layer + 1) * H]
+                groups = mode_groups(cls_l, eff, H)
+                out, nc, m = run_groups(q, ck, cv, groups, cfg.head_dim)
+                macs += m
+                if t == cfg.denoise_steps - 1:
+                    calls.append(nc)
+                    final_kv.append((k, v))
+                if classify_at == (i, t):
+                    for h in range(H):
+                        captured.append((layer, h, q[h].copy(), ck[h], region_kinds(ids[layer][h], pol[layer][h])))
+                if keep_traces:
+                    run.traces.append(LayerTrace(i, t, layer, q, k, v, out, frames, nc, m))
+                model.mix(layer, out)
+        if classify_at is not None and run.classes is None and i == classify_at[0]:
+            F = np.zeros((cfg.total_heads, 3))
+            for layer, h, qh, keys, kinds in captured:
+                F[layer * H + h] = probe_scores(qh, keys, kinds, hw, cfg.subsample_ratio, cfg.head_dim)
+            codes, obj = greedy_classify(F, cfg.dummy_count)
+            run.F, run.classes, run.objective = F, [int(c) for c in codes], obj
+            ext = extension_window(run.classes, cfg) if cfg.context_extension else None
+            for layer in range(L):
+                for h in range(H):
+                    p = derive_policy(run.classes[layer * H + h], cfg, ext)
+                    pol[layer][h] = p
+                    ids[layer][h] = rebuild(ids[layer][h], p)
+            run.cache_ratio = cache_reduction_ratio(run.classes, cfg)
+        for layer in range(L):
+            k, v = final_kv[layer]
+            for h in range(H):
+                data[(layer, h, i)] = (k[h], v[h])
+                ids[layer][h] = append(ids[layer][h], i, pol[layer][h])
+        run.frame_ids_after_step.append([[list(x) for x in lay] for lay in ids])
+        run.kernel_calls_steady = calls
+        run.step_macs.append(macs)
+    return run
+
+
+# ------------------------------------------------------------ input helper
+def round_bf16(x: np.ndarray) -> np.ndarray:
+    """Round fp64 values to bf16 (round-to-nearest-even via fp32), back to fp64.
+
+    Matches ``torch.Tensor.to(torch.bfloat16)`` of the fp32 value; used so the
+    oracle sees exactly the operands the device kernel sees.
+    """
+    f = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    u = f.view(np.uint32).astype(np.uint64)
+    lsb = (u >> np.uint64(16)) & np.uint64(1)
+    u = (u + np.uint64(0x7FFF) + lsb) & np.uint64(0xFFFF0000)
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def case_tensor(seed: int, tag: str, *idx: int, rows: int, cols: int, scale: float = 1.0) -> np.ndarray:
+    """Deterministic bf16-exact test operand from the splitmix counter PRNG."""
+    return round_bf16(matrix(derive(seed, tag, *idx), rows, cols, scale))
