@@ -70,9 +70,9 @@ int encode_rowmajor_bf16(CUtensorMap* map, const void* base, int64_t rows, int32
   return DF_OK;
 }
 
-// numpy's float64 add.reduce of a contiguous 1-D array: the first element
-// seeds the accumulator and the rest goes through pairwise_sum
-// (numpy/_core/src/umath/loops_utils.h.src, PW_BLOCKSIZE 128, 8-way unroll).
+// numpy's float64 add.reduce of a contiguous 1-D array is one pairwise_sum
+// over all n elements (numpy/_core/src/umath/loops_utils.h.src, PW_BLOCKSIZE
+// 128, 8-way unroll); verified bitwise against np.sum in tests/test_host_cpu.py.
 static double np_pairwise_sum(const double* a, int64_t n) {
   if (n < 8) {
     double res = -0.0;
@@ -95,7 +95,7 @@ static double np_pairwise_sum(const double* a, int64_t n) {
 
 static double np_sum(const std::vector<double>& v) {
   if (v.empty()) return 0.0;
-  return v[0] + np_pairwise_sum(v.data() + 1, static_cast<int64_t>(v.size()) - 1);
+  return np_pairwise_sum(v.data(), static_cast<int64_t>(v.size()));
 }
 
 }  // namespace dfb

@@ -101,10 +101,14 @@ __global__ void df_scores_kernel(const float* __restrict__ rows, const uint8_t* 
   double a0 = 0, a1 = 0, a2 = 0, cnt = 0;
   for (int r = threadIdx.x; r < hw; r += blockDim.x) {
     if (sampled[r]) {
+      // renormalise each row in fp64 so every score row sums to 1 exactly
+      // (the kernel's per-region and total sums round independently in fp32)
       const float* x = rows + (static_cast<int64_t>(h) * hw + r) * 3;
-      a0 += x[0];
-      a1 += x[1];
-      a2 += x[2];
+      const double x0 = x[0], x1 = x[1], x2 = x[2];
+      const double inv = 1.0 / (x0 + x1 + x2);
+      a0 += x0 * inv;
+      a1 += x1 * inv;
+      a2 += x2 * inv;
       cnt += 1;
     }
   }

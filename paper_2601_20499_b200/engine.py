@@ -1,0 +1,584 @@
+"""Per-layer heterogeneous attention and the AR session driver.
+
+Drop-in for the reference's engine.py (baseline_step / hma_step /
+packed_step / expected_step_macs / Session / generate_session).  Every layer
+is ONE ragged ``df_attn_fwd`` launch over all heads, whatever the mode: the
+mode only decides (a) which cache policies are legal and (b) the *logical*
+``kernel_calls`` the reference would have issued (baseline 1, hma up to 3,
+packed up to 2; engine.py:134), kept for report parity.  Physical launches are
+reported separately.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from .config import SessionConfig
+from .errors import AssignmentError, ConfigError, PackingError, ShapeError
+from .head_programming import HeadAssignment, HeadClass, greedy_classify
+from .kv_cache import (
+    CachePolicy,
+    FrameBlock,
+    HeadKVCache,
+    RingStorage,
+    as_device_bf16,
+    baseline_policy,
+    cache_stats,
+    derive_policy,
+    extension_window,
+    launch_segments,
+    rebuild_caches,
+)
+from .layout import FrameLayout
+from .profiler import Probe, subsample_rows
+
+MODES = ("baseline", "hma", "packed")
+_HMA_GROUP_ORDER = (HeadClass.DUMMY, HeadClass.SINK, HeadClass.NEIGHBOR)
+
+
+class LayerCounters:
+    """Counters of one layer call; wall time is device time (CUDA events), resolved lazily."""
+
+    __slots__ = ("kernel_calls", "key_token_macs", "physical_launches", "_events", "_wall", "_attn")
+
+    def __init__(self, kernel_calls: int = 0, key_token_macs: int = 0, physical_launches: int = 0):
+        self.kernel_calls = kernel_calls
+        self.key_token_macs = key_token_macs
+        self.physical_launches = physical_launches
+        self._events = None
+        self._wall: int | None = 0
+        self._attn: int | None = 0
+
+    def _resolve(self) -> None:
+        if self._events is not None:
+            e0, em, e1 = self._events
+            e1.synchronize()
+            self._wall = int(round(e0.elapsed_time(e1) * 1e6))
+            self._attn = int(round(em.elapsed_time(e1) * 1e6))
+            self._events = None
+
+    @property
+    def wall_time_ns(self) -> int:
+        """Device time of the layer call (current-frame staging + attention)."""
+        self._resolve()
+        return int(self._wall or 0)
+
+    @property
+    def attn_time_ns(self) -> int:
+        """Device time of the df_attn_fwd launch alone."""
+        self._resolve()
+        return int(self._attn or 0)
+
+    @wall_time_ns.setter
+    def wall_time_ns(self, v: int) -> None:
+        self._events = None
+        self._wall = int(v)
+
+    def __repr__(self) -> str:
+        return (f"LayerCounters(kernel_calls={self.kernel_calls}, key_token_macs={self.key_token_macs}, "
+                f"physical_launches={self.physical_launches})")
+
+
+@dataclass
+class StepCounters:
+    """Aggregated counters of one (AR step, denoise iteration)."""
+
+    kernel_calls: list[int] = field(default_factory=list)
+    key_token_macs: int = 0
+    physical_launches: int = 0
+    layers: list[LayerCounters] = field(default_factory=list, repr=False)
+
+    def add_layer(self, lc: LayerCounters) -> None:
+        self.kernel_calls.append(lc.kernel_calls)
+        self.key_token_macs += lc.key_token_macs
+        self.physical_launches += lc.physical_launches
+        self.layers.append(lc)
+
+    @property
+    def wall_time_ns(self) -> int:
+        return sum(lc.wall_time_ns for lc in self.layers)
+
+
+@dataclass
+class StepTrace:
+    """Per-layer observation handed to a session observer (engine.py:73-84)."""
+
+    ar_step: int
+    denoise_step: int
+    layer: int
+    q: torch.Tensor
+    outputs: torch.Tensor
+    classes: list[HeadClass] | None
+    contexts: list
+    shadow_contexts: list | None
+
+
+@dataclass
+class ProbeRequest:
+    """Fused DHP epilogue for one layer launch."""
+
+    row_sampled: torch.Tensor  # uint8 [HW]
+    probe_rows: torch.Tensor  # float32 [H, HW, 3]
+
+
+# ----------------------------------------------------------------- one layer
+def _q_rows(q_heads: torch.Tensor, H: int, hw: int, d: int, width: int, device) -> torch.Tensor:
+    q = as_device_bf16(q_heads, device)
+    if tuple(q.shape) != (H, hw, d):
+        raise ShapeError(f"q_heads shape {tuple(q.shape)} != ({H}, {hw}, {d})")
+    if d != width:
+        q = torch.nn.functional.pad(q, (0, width - d))
+    return q.reshape(H * hw, width).contiguous()
+
+
+def _dispatch(q_heads, caches: list[HeadKVCache], current_blocks: list[FrameBlock], head_dim: int,
+              groups: list[list[int]], probe: ProbeRequest | None = None, stream=None, timed: bool = True):
+    """Stage current frames, check the logical groups, launch one ragged FMHA."""
+    if stream is not None:
+        with torch.cuda.stream(stream):
+            return _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, stream, timed)
+    return _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, None, timed)
+
+
+def _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, stream, timed):
+    H = len(caches)
+    if len(current_blocks) != H:
+        raise ShapeError(f"{len(current_blocks)} current blocks for {H} caches")
+    if H == 0:
+        raise ShapeError("no heads")
+    hw = current_blocks[0].tokens
+    for b in current_blocks:
+        if b.tokens != hw:
+            raise ShapeError("current blocks of one layer must share HW")
+    for c, b in zip(caches, current_blocks):
+        c.check_current(b.frame_id)
+    n_tok = [c.context_tokens(hw) for c in caches]
+    calls = macs = 0
+    for g in groups:
+        if not g:
+            continue
+        lens = {n_tok[h] for h in g}
+        if len(lens) != 1:
+            raise PackingError(f"context lengths {sorted(lens)} differ within one batch")
+        calls += 1
+        macs += len(g) * hw * n_tok[g[0]] * head_dim
+    device = q_heads.device if isinstance(q_heads, torch.Tensor) and q_heads.is_cuda else None
+    if device is None:
+        st = next((c.storage for c in caches if c.storage is not None), None)
+        device = st.arena.device if st is not None else torch.device("cuda", torch.cuda.current_device())
+    segs = []
+    for c, b in zip(caches, current_blocks):
+        segs += c.stage_segments(b, device)
+    width = caches[0].storage.arena.width
+    q2 = _q_rows(q_heads, H, hw, head_dim, width, device)
+    d8 = ((head_dim + 7) // 8) * 8
+    out = torch.empty(H * hw, d8, dtype=torch.bfloat16, device=device)
+    work = [K.HeadWork(c.storage.arena, c.storage.base_row, n_tok[h], h, h) for h, c in enumerate(caches)]
+    pb = None
+    if probe is not None:
+        max_slots = max(c.storage.slots for c in caches)
+        tab = np.ones((H, max_slots), dtype=np.uint8)
+        for h, c in enumerate(caches):
+            tab[h, : c.storage.slots] = c.region_codes()
+        pb = K.ProbeBuffers(torch.from_numpy(tab).to(device, non_blocking=False), probe.row_sampled, probe.probe_rows)
+    lc = LayerCounters(kernel_calls=calls, key_token_macs=macs, physical_launches=1)
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    if timed:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(s)
+    if segs:
+        launch_segments(segs, s)
+        lc.physical_launches += 1
+    if timed:
+        ev[1].record(s)
+    K.attention(q2, out, work, hw, 1.0 / math.sqrt(head_dim), pb, s)
+    if timed:
+        ev[2].record(s)
+        lc._events = tuple(ev)
+    o = out.view(H, hw, d8)
+    if d8 != head_dim:
+        o = o[..., :head_dim]
+    return o, lc
+
+
+def baseline_step(q_heads, caches: list[HeadKVCache], current_blocks: list[FrameBlock], config: SessionConfig,
+                  *, stream=None, probe: ProbeRequest | None = None):
+    """Full-window attention for every head of one layer (engine.py:140-152)."""
+    for c in caches:
+        if c.policy.kind != "baseline_window":
+            raise ConfigError(f"baseline_step got a {c.policy.kind} cache")
+    return _dispatch(q_heads, caches, current_blocks, config.head_dim, [list(range(len(caches)))], probe, stream)
+
+
+def _class_groups(classes: list[HeadClass]) -> list[list[int]]:
+    return [[h for h, c in enumerate(classes) if c is want] for want in _HMA_GROUP_ORDER]
+
+
+def hma_step(q_heads, caches, current_blocks, classes: list[HeadClass], config: SessionConfig, *, stream=None,
+             probe: ProbeRequest | None = None):
+    """Class-specific contexts; logically one call per class present (engine.py:161-174)."""
+    if len(classes) != len(caches):
+        raise AssignmentError(f"{len(classes)} classes for {len(caches)} heads in this layer")
+    return _dispatch(q_heads, caches, current_blocks, config.head_dim, _class_groups(list(classes)), probe, stream)
+
+
+def packed_step(q_heads, caches, current_blocks, classes: list[HeadClass], config: SessionConfig, *, stream=None,
+                probe: ProbeRequest | None = None):
+    """Dummy+sink share one logical call, neighbors the other (engine.py:177-195)."""
+    if not config.packing_enabled:
+        raise ConfigError("packed_step requires packing_enabled")
+    if len(classes) != len(caches):
+        raise AssignmentError(f"{len(classes)} classes for {len(caches)} heads in this layer")
+    ds = [h for h, c in enumerate(classes) if c is not HeadClass.NEIGHBOR]
+    nb = [h for h, c in enumerate(classes) if c is HeadClass.NEIGHBOR]
+    return _dispatch(q_heads, caches, current_blocks, config.head_dim, [ds, nb], probe, stream)
+
+
+def expected_step_macs(config: SessionConfig, mode: str, history_frames: int,
+                       assignment: HeadAssignment | None = None) -> int:
+    """Closed-form key-token MACs of one denoise iteration (engine.py:198-237)."""
+    if mode not in MODES:
+        raise ConfigError(f"unknown mode {mode!r}")
+    ext = extension_window(assignment, config) if (assignment is not None and config.context_extension) else None
+
+    def past(p: CachePolicy) -> int:
+        h = history_frames
+        if h == 0:
+            return 0
+        sink_seen = p.sink_frame < h
+        if p.kind == "baseline_window":
+            return min(h - 1 if sink_seen else h, p.window_len - 1) + (1 if sink_seen else 0)
+        if p.kind == "sink_only":
+            return 1 if sink_seen else 0
+        return min(h, p.recent_capacity)
+
+    if mode == "baseline" or assignment is None:
+        ctxs = [(past(baseline_policy(config)) + 1) * config.HW] * config.total_heads
+    else:
+        ctxs = [(past(derive_policy(c, config, extended_window=ext)) + 1) * config.HW for c in assignment.classes]
+    return sum(config.HW * c * config.head_dim for c in ctxs)
+
+
+# ------------------------------------------------------------------- session
+@dataclass
+class RunReport:
+    mode: str
+    config: dict
+    cache_reduction_ratio: float
+    assignment: dict | None
+    steps: list[dict]
+    kernel_calls_steady: list[int]
+    total_key_token_macs: int
+    total_wall_time_ns: int
+    output_digest: str
+    physical_launches_steady: list[int] = field(default_factory=list)
+
+    def to_dict(self) -> dict:
+        return {
+            "mode": self.mode,
+            "config": self.config,
+            "cache_reduction_ratio": self.cache_reduction_ratio,
+            "assignment": self.assignment,
+            "steps": self.steps,
+            "kernel_calls_steady": self.kernel_calls_steady,
+            "total_key_token_macs": self.total_key_token_macs,
+            "total_wall_time_ns": self.total_wall_time_ns,
+            "output_digest": self.output_digest,
+            "physical_launches_steady": self.physical_launches_steady,
+        }
+
+
+def _digest(frames) -> str:
+    h = hashlib.sha256()
+    for x in frames:
+        if x is None:
+            continue
+        t = x if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x))
+        t = t.detach().contiguous().cpu()
+        h.update(str(tuple(t.shape)).encode())
+        h.update(t.view(torch.uint8).numpy().tobytes() if t.dtype != torch.bool else t.numpy().tobytes())
+    return h.hexdigest()
+
+
+class Session:
+    """One generation run on the device (engine.py:268-576).
+
+    The model protocol is the reference's: ``frame_input(ar, t)``,
+    ``qkv(layer, x, ar, t) -> (q, k, v)`` each (heads, HW, head_dim) (torch
+    CUDA tensors preferred; host arrays are uploaded), and ``mix(layer,
+    outputs)`` whose result is added to ``x`` (None = open loop).
+    """
+
+    def __init__(self, model, config: SessionConfig, mode: str = "baseline",
+                 observer: Callable[[StepTrace], None] | None = None, shadow: bool = False,
+                 device: torch.device | str | None = None, stream: torch.cuda.Stream | None = None):
+        if mode not in MODES:
+            raise ConfigError(f"unknown mode {mode!r}, expected one of {MODES}")
+        if mode == "packed" and not config.packing_enabled:
+            raise ConfigError("packed mode requires packing_enabled")
+        if mode == "packed" and config.merged_window is not None:
+            raise ConfigError("merged_window gives sink heads a context longer than packed "
+                              "dummy heads; packing requires the plain sink policy")
+        self.model = model
+        self.config = config
+        self.mode = mode
+        self.observer = observer
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.stream = stream
+        self.assignment: HeadAssignment | None = None
+        self.objective: float | None = None
+        self.pack_stats: dict | None = None
+        self._next_step = 0
+        self._frames: list = []
+        self._step_counters: list[tuple[int, list[StepCounters]]] = []
+        self._kernel_calls_last: list[int] = []
+        self._phys_last: list[int] = []
+        self._probe_requests: dict[tuple[int, int], set[float]] = {}
+        self._probe_tables: dict[tuple[int, int, float], np.ndarray] = {}
+        self._classify_at: tuple[int, int] | None = None
+        if mode != "baseline" and config.dummy_count > 0 and config.probe_ar_step < config.ar_steps:
+            self._classify_at = self._probe_key(None)
+            self._probe_requests.setdefault(self._classify_at, set()).add(config.subsample_ratio)
+        self.caches = self._fresh_caches()
+        self._shadow = shadow and mode != "baseline"
+        self.shadow_caches = self._fresh_caches() if self._shadow else None
+
+    def _fresh_caches(self) -> list[list[HeadKVCache]]:
+        cfg = self.config
+        pol = baseline_policy(cfg)
+        per = K.KVArena.region_rows(pol.ring_slots * cfg.HW)
+        arena = K.KVArena(per * cfg.total_heads, K.padded_width(cfg.head_dim), self.device)
+        return [[HeadKVCache(pol, storage=RingStorage(arena, arena.allocate(pol.ring_slots * cfg.HW), pol.ring_slots,
+                                                      cfg.HW, cfg.head_dim))
+                 for _ in range(cfg.num_heads)] for _ in range(cfg.num_layers)]
+
+    # ------------------------------------------------------------ probe
+    def _probe_key(self, probe: Probe | None) -> tuple[int, int]:
+        if probe is None:
+            probe = Probe(self.config.probe_ar_step, self.config.probe_denoise_step)
+        dn = probe.denoise_step if probe.denoise_step is not None else self.config.denoise_steps - 1
+        if not 0 <= dn < self.config.denoise_steps:
+            raise ConfigError(f"probe denoise step {dn} out of range")
+        if not 0 <= probe.ar_step < self.config.ar_steps:
+            raise ConfigError(f"probe AR step {probe.ar_step} out of range")
+        return probe.ar_step, dn
+
+    def probe_scores(self, probe: Probe | None = None, subsample_ratio: float | None = None) -> np.ndarray:
+        """(total_heads, 3) region scores at the probe (runs forward if needed)."""
+        ratio = self.config.subsample_ratio if subsample_ratio is None else subsample_ratio
+        subsample_rows(self.config.HW, ratio)  # validates (ConfigError)
+        key = self._probe_key(probe)
+        if (key[0], key[1], ratio) not in self._probe_tables:
+            if self._next_step > key[0]:
+                raise ConfigError(f"session already advanced past AR step {key[0]}")
+            if self._classify_at is not None and key[0] > self._classify_at[0]:
+                raise ConfigError("probe lies beyond the classification step of this session")
+            self._probe_requests.setdefault(key, set()).add(ratio)
+            while self._next_step <= key[0]:
+                self._run_step(self._next_step)
+        return self._probe_tables[(key[0], key[1], ratio)]
+
+    # ------------------------------------------------------------ stepping
+    def _effective_mode(self) -> str:
+        return "baseline" if (self.mode == "baseline" or self.assignment is None) else self.mode
+
+    def _classes_for_layer(self, layer: int) -> list[HeadClass]:
+        h = self.config.num_heads
+        return list(self.assignment.classes[layer * h : (layer + 1) * h])
+
+    def _layer_attention(self, layer, q, caches, current_blocks, probe=None):
+        mode = self._effective_mode()
+        if mode == "baseline":
+            return baseline_step(q, caches, current_blocks, self.config, stream=self.stream, probe=probe)
+        classes = self._classes_for_layer(layer)
+        if mode == "hma":
+            return hma_step(q, caches, current_blocks, classes, self.config, stream=self.stream, probe=probe)
+        return packed_step(q, caches, current_blocks, classes, self.config, stream=self.stream, probe=probe)
+
+    def _classify(self) -> None:
+        cfg = self.config
+        key = self._classify_at
+        table = self._probe_tables[(key[0], key[1], cfg.subsample_ratio)]
+        self.assignment, self.objective = greedy_classify(table, cfg.dummy_count)
+        ext = extension_window(self.assignment, cfg) if cfg.context_extension else None
+        flat_caches = [c for layer in self.caches for c in layer]
+        policies = [derive_policy(c, cfg, extended_window=ext) for c in self.assignment.classes]
+        rows = sum(K.KVArena.region_rows(p.ring_slots * cfg.HW) for p in policies)
+        arena = K.KVArena(rows, K.padded_width(cfg.head_dim), self.device)
+        s = self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        new = rebuild_caches(flat_caches, policies, arena, stream=s)
+        e1.record(s)
+        moved = sum(len(c) for c in new) * cfg.HW * arena.width * 2 * 2 * 2  # K+V, read+write
+        self.pack_stats = {"bytes": moved, "events": (e0, e1)}
+        H = cfg.num_heads
+        self.caches = [new[l * H : (l + 1) * H] for l in range(cfg.num_layers)]
+
+    def _probe_buffers(self, ratio: float) -> ProbeRequest:
+        cfg = self.config
+        rows = subsample_rows(cfg.HW, ratio)
+        flags = torch.zeros(cfg.HW, dtype=torch.uint8)
+        flags[torch.from_numpy(rows)] = 1
+        return ProbeRequest(flags.to(self.device), torch.zeros(cfg.num_heads, cfg.HW, 3, dtype=torch.float32,
+                                                                device=self.device))
+
+    def _finalize_probe(self, key, ratio, per_layer: list[ProbeRequest]) -> None:
+        tables = []
+        for pr in per_layer:
+            F = K.scores_finalize(K.ProbeBuffers(None, pr.row_sampled, pr.probe_rows), self.stream)
+            tables.append(F)
+        self._probe_tables[(key[0], key[1], ratio)] = torch.cat(tables).cpu().numpy()
+
+    def _model_qkv(self, layer, x, ar, t):
+        q, k, v = self.model.qkv(layer, x, ar, t)
+        return as_device_bf16(q, self.device), as_device_bf16(k, self.device), as_device_bf16(v, self.device)
+
+    def _run_step(self, ar_step: int) -> None:
+        cfg = self.config
+        final_kv = []
+        step_counters: list[StepCounters] = []
+        x = None
+        for t in range(cfg.denoise_steps):
+            x = self.model.frame_input(ar_step, t)
+            final = t == cfg.denoise_steps - 1
+            ratios = sorted(self._probe_requests.get((ar_step, t), ()))
+            probes: dict[float, list[ProbeRequest]] = {r: [] for r in ratios}
+            counters = StepCounters()
+            for layer in range(cfg.num_layers):
+                q, k, v = self._model_qkv(layer, x, ar_step, t)
+                blocks = [FrameBlock(ar_step, k[h], v[h]) for h in range(cfg.num_heads)]
+                pr = None
+                if ratios:
+                    pr = self._probe_buffers(ratios[0])
+                    probes[ratios[0]].append(pr)
+                outputs, lc = self._layer_attention(layer, q, self.caches[layer], blocks, pr)
+                for extra in ratios[1:]:  # another ratio at the same key: re-run the probe epilogue
+                    pe = self._probe_buffers(extra)
+                    probes[extra].append(pe)
+                    self._layer_attention(layer, q, self.caches[layer], blocks, pe)
+                counters.add_layer(lc)
+                if self.observer is not None:
+                    self._notify(ar_step, t, layer, q, outputs, blocks)
+                if final:
+                    final_kv.append(blocks)
+                m = self.model.mix(layer, outputs)
+                if m is not None:
+                    x = m if x is None else x + m
+            for r in ratios:
+                self._finalize_probe((ar_step, t), r, probes[r])
+            step_counters.append(counters)
+        if self._classify_at is not None and self.assignment is None and ar_step == self._classify_at[0]:
+            self._classify()
+        s = self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
+        segs = []
+        for layer in range(cfg.num_layers):
+            for h, block in enumerate(final_kv[layer]):
+                segs += self.caches[layer][h].append_segments(block, self.device)
+                if self.shadow_caches is not None:
+                    segs += self.shadow_caches[layer][h].append_segments(block, self.device)
+        if segs:
+            launch_segments(segs, s)
+        self._frames.append(x)
+        self._step_counters.append((ar_step, step_counters))
+        self._kernel_calls_last = list(step_counters[-1].kernel_calls)
+        self._phys_last = [lc.physical_launches for lc in step_counters[-1].layers]
+        self._next_step = ar_step + 1
+
+    def _notify(self, ar_step, t, layer, q, outputs, blocks) -> None:
+        contexts = []
+        for c, b in zip(self.caches[layer], blocks):
+            keys, values, lay = c.gather_context(b)
+            contexts.append((keys, values, lay, c.frame_ids + [b.frame_id]))
+        shadow = None
+        if self.shadow_caches is not None:
+            shadow = []
+            for c, b in zip(self.shadow_caches[layer], blocks):
+                keys, values, _ = c.gather_context(b)
+                shadow.append((keys, values, c.frame_ids + [ar_step]))
+        classes = self._classes_for_layer(layer) if self._effective_mode() != "baseline" else None
+        self.observer(StepTrace(ar_step, t, layer, q, outputs, classes, contexts, shadow))
+
+    def run(self):
+        while self._next_step < self.config.ar_steps:
+            self._run_step(self._next_step)
+        return self._frames, self._report()
+
+    def time_step(self, reps: int = 5) -> dict:
+        """Re-dispatch the next step's final denoise iteration ``reps`` times (engine.py:511-550).
+
+        Device-timed (CUDA events); the session does not advance.
+        """
+        if reps < 1:
+            raise ConfigError("reps must be >= 1")
+        cfg = self.config
+        ar_step = self._next_step
+        t = cfg.denoise_steps - 1
+        walls = []
+        counters = StepCounters()
+        for _ in range(reps):
+            counters = StepCounters()
+            x = self.model.frame_input(ar_step, t)
+            for layer in range(cfg.num_layers):
+                q, k, v = self._model_qkv(layer, x, ar_step, t)
+                blocks = [FrameBlock(ar_step, k[h], v[h]) for h in range(cfg.num_heads)]
+                outputs, lc = self._layer_attention(layer, q, self.caches[layer], blocks)
+                counters.add_layer(lc)
+                m = self.model.mix(layer, outputs)
+                if m is not None:
+                    x = m if x is None else x + m
+            walls.append(counters.wall_time_ns)
+        walls.sort()
+        mid = len(walls) // 2
+        median = walls[mid] if len(walls) % 2 else (walls[mid - 1] + walls[mid]) // 2
+        return {"wall_time_ns_median": int(median), "key_token_macs": counters.key_token_macs,
+                "kernel_calls_per_layer": counters.kernel_calls,
+                "physical_launches_per_layer": [lc.physical_launches for lc in counters.layers]}
+
+    def _report(self) -> RunReport:
+        cfg = self.config
+        if self.assignment is not None:
+            ratio = cache_stats(self.assignment, cfg).reduction_ratio
+            assignment = {
+                "n_dummy": self.assignment.dummy_count,
+                "objective": self.objective,
+                "counts": self.assignment.counts(),
+                "per_layer": self.assignment.per_layer_histogram(cfg.num_heads),
+                "heads": self.assignment.to_records(cfg.num_heads),
+            }
+        else:
+            ratio, assignment = 1.0, None
+        steps = []
+        for ar, scs in self._step_counters:
+            steps.append({
+                "ar_step": ar,
+                "key_token_macs": sum(sc.key_token_macs for sc in scs),
+                "kernel_calls_per_layer": list(scs[-1].kernel_calls),
+                "wall_time_ns": sum(sc.wall_time_ns for sc in scs),
+                "layer_wall_time_ns": [lc.wall_time_ns for sc in scs for lc in sc.layers],
+            })
+        return RunReport(
+            mode=self.mode,
+            config=cfg.to_dict(),
+            cache_reduction_ratio=ratio,
+            assignment=assignment,
+            steps=steps,
+            kernel_calls_steady=self._kernel_calls_last,
+            total_key_token_macs=sum(s["key_token_macs"] for s in steps),
+            total_wall_time_ns=sum(s["wall_time_ns"] for s in steps),
+            output_digest=_digest(self._frames),
+            physical_launches_steady=self._phys_last,
+        )
+
+
+def generate_session(model, config: SessionConfig, mode: str = "baseline",
+                     observer: Callable[[StepTrace], None] | None = None, shadow: bool = False, **kw):
+    """Run a full session; returns (per-step frame outputs, report)."""
+    return Session(model, config, mode, observer=observer, shadow=shadow, **kw).run()

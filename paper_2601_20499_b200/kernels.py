@@ -119,14 +119,24 @@ def attention(
     """
     if not work:
         return
-    if len(work) > _lib.DF_MAX_HEADS:
-        # more heads than one launch carries: split (still one stream, in order)
-        for i in range(0, len(work), _lib.DF_MAX_HEADS):
+    # One launch carries <= DF_MAX_HEADS heads from <= DF_MAX_ARENAS arenas;
+    # split contiguous runs otherwise (sessions use one arena: one launch).
+    chunks, cur, seen = [], [], set()
+    for i, w in enumerate(work):
+        new_arena = id(w.arena) not in seen
+        if cur and (len(cur) == _lib.DF_MAX_HEADS or (new_arena and len(seen) == _lib.DF_MAX_ARENAS)):
+            chunks.append(cur)
+            cur, seen = [], set()
+        cur.append(i)
+        seen.add(id(w.arena))
+    chunks.append(cur)
+    if len(chunks) > 1:
+        for c in chunks:
+            sl = slice(c[0], c[-1] + 1)
             sub_probe = None
             if probe is not None:
-                sl = slice(i, i + _lib.DF_MAX_HEADS)
                 sub_probe = ProbeBuffers(probe.region_of_slot[sl], probe.row_sampled, probe.probe_rows[sl])
-            attention(q, out, work[i : i + _lib.DF_MAX_HEADS], hw, scale, sub_probe, stream)
+            attention(q, out, work[sl], hw, scale, sub_probe, stream)
         return
     if q.dtype != torch.bfloat16 or out.dtype != torch.bfloat16:
         raise ShapeError("q and out must be bfloat16")

@@ -1,0 +1,213 @@
+"""Device path (libdfb200 via the public API) against the reference's golden
+vectors and the CPU oracle fed the same bf16 operands.
+
+Tolerance for attention outputs (north star): per-head normwise
+max|o - o_ref| / max|o_ref| <= 2e-2, with the reference evaluated in fp64 on
+the bf16-rounded operands.  Classes, frame ids, group counters: exact.
+DHP scores: |dF| <= 1e-3.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2601_20499_b200 as df
+from oracle import df_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+G = os.path.join(os.path.dirname(__file__), "golden")
+TOL = 2e-2
+DEV = torch.device("cuda:0")
+NAME_TO = {"sink": df.HeadClass.SINK, "neighbor": df.HeadClass.NEIGHBOR, "dummy": df.HeadClass.DUMMY}
+CODES = (df.HeadClass.SINK, df.HeadClass.NEIGHBOR, df.HeadClass.DUMMY)
+
+
+def normwise(got, ref):
+    got = got.float().cpu().numpy() if isinstance(got, torch.Tensor) else np.asarray(got)
+    ref = np.asarray(ref)
+    return [float(np.abs(got[h] - ref[h]).max() / max(np.abs(ref[h]).max(), 1e-30)) for h in range(ref.shape[0])]
+
+
+def dev(x):
+    return torch.tensor(x, dtype=torch.float32).to(DEV).to(torch.bfloat16)
+
+
+def test_step_functions_match_reference_goldens():
+    meta = json.load(open(os.path.join(G, "attention.json")))
+    arr = np.load(os.path.join(G, "attention.npz"))
+    for rec in meta:
+        H, HW, d, hist = rec["H"], rec["HW"], rec["d"], rec["history"]
+        cfg = df.SessionConfig(num_layers=1, num_heads=H, head_dim=d, HW=HW, window_len=rec["W"],
+                               ar_steps=hist + 1, packing_enabled=rec["packing"])
+        q = dev(np.stack([O.case_tensor(rec["seed"], "q", h, rows=HW, cols=d, scale=rec["q_scale"]) for h in range(H)]))
+        kv = {(h, f): (dev(O.case_tensor(rec["seed"], "k", h, f, rows=HW, cols=d)),
+                       dev(O.case_tensor(rec["seed"], "v", h, f, rows=HW, cols=d)))
+              for h in range(H) for f in range(hist + 1)}
+        base = []
+        for h in range(H):
+            c = df.HeadKVCache(df.baseline_policy(cfg))
+            for f in range(hist):
+                c.append_and_evict(df.FrameBlock(f, *kv[(h, f)]))
+            base.append(c)
+        cur = [df.FrameBlock(hist, *kv[(h, hist)]) for h in range(H)]
+        classes = [NAME_TO[c] for c in rec["classes"]]
+        pruned = [c.rebuild(df.derive_policy(x, cfg)) for c, x in zip(base, classes)]
+        for mode, want in rec["modes"].items():
+            if mode == "baseline":
+                out, lc = df.baseline_step(q, base, cur, cfg)
+                caches = base
+            elif mode == "hma":
+                out, lc = df.hma_step(q, pruned, cur, classes, cfg)
+                caches = pruned
+            else:
+                out, lc = df.packed_step(q, pruned, cur, classes, cfg)
+                caches = pruned
+            assert [c.frame_ids + [hist] for c in caches] == want["frames"], (rec["name"], mode)
+            assert lc.kernel_calls == want["kernel_calls"], (rec["name"], mode)
+            assert lc.key_token_macs == want["key_token_macs"]
+            assert lc.physical_launches >= 1
+            errs = normwise(out, arr[f"{rec['name']}/{mode}"])
+            assert max(errs) <= TOL, (rec["name"], mode, errs)
+
+
+def _planted_session(rec):
+    cfg = df.SessionConfig(**rec["config"])
+    stream = O.PlantedStream(rec["labels"], 2.0, rec["noise_seed"], O.Config(**rec["config"]))
+    return cfg, stream
+
+
+def test_planted_sessions_match_reference():
+    """Classes bit-exact, F within 1e-3, frame ids / counters / ratio exact (seeds 0-5, ratios 1 and 0.25)."""
+    for rec in json.load(open(os.path.join(G, "planted_sessions.json"))):
+        cfg, stream = _planted_session(rec)
+        s = df.Session(stream, cfg, rec["mode"])
+        frames, rep = s.run()
+        assert [df.head_programming.CODE_OF[c] for c in s.assignment.classes] == rec["classes"], rec["seed"]
+        key = (cfg.probe_ar_step, cfg.denoise_steps - 1, cfg.subsample_ratio)
+        F = s._probe_tables[key]
+        assert np.abs(F - np.array(rec["F"])).max() <= 1e-3
+        assert rep.cache_reduction_ratio == rec["cache_reduction_ratio"]
+        assert rep.kernel_calls_steady == rec["kernel_calls_steady"]
+        assert [st["key_token_macs"] for st in rep.steps] == rec["step_macs"]
+        assert [[c.frame_ids for c in layer] for layer in s.caches] == rec["frame_ids"]
+        assert all(p == 2 for p in rep.physical_launches_steady)  # append + ONE attention launch per layer
+        assert s.objective == pytest.approx(rec["objective"], abs=1e-3)
+
+
+def test_session_layer_outputs_match_oracle_on_device_operands():
+    """Observer pattern: each layer's device output vs fp64 attention on the
+    device's own bf16 context, C1-like shape (HW 192, d 64, W 6, 10 steps, 2 denoise)."""
+    ocfg = O.Config(num_layers=2, num_heads=8, head_dim=64, HW=192, window_len=6, ar_steps=10, denoise_steps=2,
+                    dummy_count=6, probe_ar_step=2, subsample_ratio=0.25)
+    labels = ("sink", "neighbor", "current", "current", "neighbor", "sink", "neighbor", "current") * 2
+    stream = O.PlantedStream(labels, 2.0, O.derive(3, "planted"), ocfg)
+    cfg = df.SessionConfig(**ocfg.__dict__)
+    worst = []
+
+    def observer(tr):
+        for h, (keys, values, layout, frames) in enumerate(tr.contexts):
+            qh = tr.q[h].double().cpu().numpy()
+            k = keys.double().cpu().numpy()
+            v = values.double().cpu().numpy()
+            ref = O.batched_attention(qh[None], k[None], v[None], 1 / math.sqrt(cfg.head_dim))[0]
+            got = tr.outputs[h].float().cpu().numpy()
+            worst.append(np.abs(got - ref).max() / np.abs(ref).max())
+
+    s = df.Session(stream, cfg, "packed", observer=observer)
+    s.run()
+    assert max(worst) <= TOL
+    want = ["sink" if c is df.HeadClass.SINK else "neighbor" if c is df.HeadClass.NEIGHBOR else "current"
+            for c in s.assignment.classes]
+    assert want == list(labels)  # planted labels recovered at margin 2
+
+
+def test_probe_scores_match_oracle_at_wan_like_shape():
+    """Fused DHP epilogue vs the oracle's explicit map at HW 1560 (partial kv tiles, 2-slot tiles)."""
+    ocfg = O.Config(num_layers=1, num_heads=6, head_dim=128, HW=1560, window_len=4, ar_steps=3, denoise_steps=1,
+                    dummy_count=2, probe_ar_step=2, subsample_ratio=0.25)
+    labels = ("sink", "neighbor", "current", "sink", "neighbor", "current")
+    stream = O.PlantedStream(labels, 1.0, O.derive(9, "planted"), ocfg)
+    cfg = df.SessionConfig(**ocfg.__dict__)
+    run = O.run_session(stream, ocfg, "hma", qkv_hook=lambda l, i, t, q, k, v: (O.round_bf16(q), O.round_bf16(k),
+                                                                                     O.round_bf16(v)))
+    s = df.Session(stream, cfg, "hma")
+    s.run()
+    F = s._probe_tables[(2, 0, 0.25)]
+    assert np.abs(F - run.F).max() <= 1e-3
+    assert [df.head_programming.CODE_OF[c] for c in s.assignment.classes] == run.classes
+
+
+def test_rebuild_pack_moves_exact_bytes():
+    ocfg = O.Config(num_layers=2, num_heads=4, head_dim=128, HW=300, window_len=4, ar_steps=6, denoise_steps=1,
+                    dummy_count=3, probe_ar_step=4)
+    labels = ("sink", "neighbor", "current", "neighbor", "current", "sink", "neighbor", "current")
+    stream = O.PlantedStream(labels, 2.0, O.derive(5, "planted"), ocfg)
+    cfg = df.SessionConfig(**ocfg.__dict__)
+    s = df.Session(stream, cfg, "packed")
+    s.run()
+    for layer in range(2):
+        for h in range(4):
+            for b in s.caches[layer][h].blocks:
+                _, k, v = stream.qkv(layer, None, b.frame_id, 0)
+                assert torch.equal(b.keys.cpu(), dev(k[h]).cpu())
+                assert torch.equal(b.values.cpu(), dev(v[h]).cpu())
+
+
+def test_error_mapping_matches_reference_exceptions():
+    cfg = df.SessionConfig(num_layers=1, num_heads=2, head_dim=64, HW=64, window_len=3, ar_steps=6)
+    blk = lambda f: df.FrameBlock(f, torch.randn(64, 64, device=DEV), torch.randn(64, 64, device=DEV))
+    q = torch.randn(2, 64, 64, device=DEV)
+    sink = df.HeadKVCache(df.CachePolicy("sink_only", 3))
+    sink.append_and_evict(blk(0))
+    dummy = df.HeadKVCache(df.CachePolicy("dummy_empty", 3))
+    with pytest.raises(df.PackingError):
+        df.packed_step(q, [sink, dummy], [blk(1), blk(1)], [df.HeadClass.SINK, df.HeadClass.DUMMY], cfg)
+    with pytest.raises(df.ConfigError):
+        df.baseline_step(q, [sink, dummy], [blk(1), blk(1)], cfg)
+    with pytest.raises(df.AssignmentError):
+        df.hma_step(q, [sink, dummy], [blk(1), blk(1)], [df.HeadClass.SINK], cfg)
+    with pytest.raises(df.OrderingError):
+        df.hma_step(q, [sink, dummy], [blk(0), blk(0)], [df.HeadClass.SINK, df.HeadClass.DUMMY], cfg)
+    with pytest.raises(df.ConfigError):
+        df.packed_step(q, [sink, dummy], [blk(1), blk(1)], [df.HeadClass.SINK, df.HeadClass.DUMMY],
+                       df.SessionConfig(**{**cfg.to_dict(), "packing_enabled": False}))
+
+
+def test_wan_layer_full_size_properties():
+    """BASELINE config 1 shape (HW 4680, d 128, W 6 warm): output vs fp32 torch on sampled heads,
+    hma == packed bitwise, run-to-run determinism, 1 attention launch per layer."""
+    H, HW, d, W = 12, 4680, 128, 6
+    cfg = df.SessionConfig(num_layers=1, num_heads=H, head_dim=d, HW=HW, window_len=W, ar_steps=8, dummy_count=6)
+    g = torch.Generator(device=DEV).manual_seed(0)
+    frames = {(h, f): (torch.randn(HW, d, device=DEV, generator=g).to(torch.bfloat16),
+                       torch.randn(HW, d, device=DEV, generator=g).to(torch.bfloat16)) for h in range(H) for f in range(8)}
+    base = []
+    for h in range(H):
+        c = df.HeadKVCache(df.baseline_policy(cfg))
+        for f in range(7):
+            c.append_and_evict(df.FrameBlock(f, *frames[(h, f)]))
+        base.append(c)
+    q = torch.randn(H, HW, d, device=DEV, generator=g).to(torch.bfloat16)
+    cur = [df.FrameBlock(7, *frames[(h, 7)]) for h in range(H)]
+    out, lc = df.baseline_step(q, base, cur, cfg)
+    out2, _ = df.baseline_step(q, base, cur, cfg)
+    assert torch.equal(out, out2)
+    for h in (0, 7):
+        k, v, _ = base[h].gather_context(cur[h])
+        ref = torch.softmax((q[h].float() @ k.float().T) / math.sqrt(d), -1) @ v.float()
+        assert (out[h].float() - ref).abs().max() / ref.abs().max() <= TOL
+    classes = [df.HeadClass.DUMMY] * 6 + [df.HeadClass.SINK] * 3 + [df.HeadClass.NEIGHBOR] * 3
+    pruned = df.rebuild_caches(base, [df.derive_policy(c, cfg) for c in classes])
+    o_h, lh = df.hma_step(q, pruned, cur, classes, cfg)
+    o_p, lp = df.packed_step(q, pruned, cur, classes, cfg)
+    assert torch.equal(o_h, o_p)
+    assert (lh.kernel_calls, lp.kernel_calls) == (3, 2)
+    assert lp.key_token_macs * 4 == 4 * d * HW * (9 * 2 * HW + 3 * 6 * HW)
+    for h in (0, 6, 11):
+        k, v, _ = pruned[h].gather_context(cur[h])
+        ref = torch.softmax((q[h].float() @ k.float().T) / math.sqrt(d), -1) @ v.float()
+        assert (o_p[h].float() - ref).abs().max() / ref.abs().max() <= TOL
