@@ -77,7 +77,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
         return self
@@ -278,13 +278,11 @@ def gpu_arm(args, ws, rank, local):
     pack_ms = []
     new = None
     for _ in range(3):
+        stats: dict = {}
+        new = df.rebuild_caches(flat, pols, stats=stats)
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        new = df.rebuild_caches(flat, pols)
-        e1.record()
-        torch.cuda.synchronize()
-        pack_ms.append(e0.elapsed_time(e1))
+        pack_ms.append(stats["events"][0].elapsed_time(stats["events"][1]))
+        del stats
     retained = sum(len(c) for c in new)
     pack_bytes = retained * HW * D * 2 * 2 * 2  # frames x (K,V) x (read+write)
     packed = [new[l * H:(l + 1) * H] for l in range(L)]
@@ -363,7 +361,7 @@ def gpu_arm(args, ws, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")

@@ -96,8 +96,10 @@ typedef struct df_attn_args {
   const uint8_t* region_of_slot;  /* probe, device [num_heads][max_slots]; 0 sink 1 neighbor 2 current */
   const uint8_t* row_sampled;     /* probe, device [hw] (profiler.py:132-144) */
   float* probe_rows;              /* probe, device [num_heads][hw][3] region masses per sampled row */
-  int32_t kv_split;               /* reserved, 0 */
-  int32_t reserved;
+  /* Split-KV workspace (device, caller-owned, zero-filled once; the kernel
+   * leaves its counters at zero).  NULL or too small => no kv splitting. */
+  void* workspace;
+  int64_t workspace_bytes;
 } df_attn_args;
 
 /* A row-strided device copy: `rows` rows of `row_bytes` bytes. row_bytes and
@@ -113,6 +115,9 @@ typedef struct df_copy_seg {
 
 /* ---- attention (tcgen05 / TMEM / TMA, sm_100a) ---- */
 DF_API int df_attn_fwd(const df_attn_args* args, void* stream);
+/* Workspace df_attn_fwd would use for these heads (LPT split plan over the
+ * device's SMs); 0 when no head is split. */
+DF_API int df_attn_workspace_bytes(const df_attn_args* args, int64_t* bytes);
 
 /* TMA descriptors (K map then V map, 2*DF_TMAP_BYTES bytes) of an arena whose
  * K and V planes are device bf16 [rows][head_dim]. */

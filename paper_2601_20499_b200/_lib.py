@@ -14,7 +14,7 @@ import threading
 from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdfb200.so")
+LIB_PATH = os.environ.get("DF_LIB_PATH") or os.path.join(_HERE, "libdfb200.so")  # env: dev A/B builds only
 
 DF_OK = 0
 DF_E_SHAPE = 1
@@ -71,8 +71,8 @@ class AttnArgs(ctypes.Structure):
         ("region_of_slot", ctypes.c_void_p),
         ("row_sampled", ctypes.c_void_p),
         ("probe_rows", ctypes.c_void_p),
-        ("kv_split", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("workspace", ctypes.c_void_p),
+        ("workspace_bytes", ctypes.c_int64),
     ]
 
 
@@ -90,6 +90,7 @@ class CopySeg(ctypes.Structure):
 # Every symbol include/df_b200.h declares, with its ctypes signature.
 _SIGNATURES = {
     "df_attn_fwd": (ctypes.c_int, [ctypes.POINTER(AttnArgs), ctypes.c_void_p]),
+    "df_attn_workspace_bytes": (ctypes.c_int, [ctypes.POINTER(AttnArgs), ctypes.POINTER(ctypes.c_int64)]),
     "df_kv_arena_maps": (
         ctypes.c_int,
         [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p],

@@ -30,7 +30,11 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <numeric>
+#include <queue>
+#include <vector>
 
 #include "df_internal.h"
 #include "df_ptx.cuh"
@@ -42,6 +46,10 @@ constexpr int kBN = 128;        // keys per kv tile
 constexpr int kWarps = 12;  // see role map above
 constexpr int kThreads = kWarps * 32;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+#ifndef DF_EMU_EVERY
+#define DF_EMU_EVERY 4
+#endif
+constexpr int kEmuEvery = DF_EMU_EVERY;  // 1 in kEmuEvery exp2 pairs runs as a polynomial on the FMA pipe
 
 struct HeadParam {
   int32_t base_row;
@@ -49,7 +57,9 @@ struct HeadParam {
   int16_t q_head;
   int16_t o_head;
   int16_t arena;
-  int16_t pad;
+  int16_t n_split;      // kv pieces per query-tile pair (1 = no split)
+  int32_t part_base;    // first partial slot of this head (split heads)
+  int32_t group_base;   // first combine counter of this head (split heads)
 };
 
 struct __align__(64) AttnParams {
@@ -59,6 +69,9 @@ struct __align__(64) AttnParams {
   const uint8_t* region_tab;
   const uint8_t* row_sampled;
   float* probe_rows;
+  float* ws_o;           // split partials: [slot][256][D] unnormalised O
+  float* ws_ml;          // [slot][256][2] (running max in log2 units, row sum)
+  int32_t* ws_cnt;       // [group] arrival counters (zero between launches)
   int64_t out_ld;
   int32_t hw;
   int32_t d_out;
@@ -66,6 +79,7 @@ struct __align__(64) AttnParams {
   int32_t n_qpairs;
   int32_t max_slots;
   float scale_log2;
+  int32_t item_prefix[DF_MAX_HEADS + 1];  // CTAs before head rank r (LPT order)
   uint8_t head_order[DF_MAX_HEADS];
   HeadParam heads[DF_MAX_HEADS];
 };
@@ -82,9 +96,13 @@ struct AttnCfg {
   static constexpr int kVOff = kKOff + kStagesK * kTileBytes;
   static constexpr int kBarOff = kVOff + kStagesV * kTileBytes;
   static constexpr int kNumBars = 1 + 2 * kStagesK + 2 * kStagesV + 6;
-  static constexpr int kSmem = kBarOff + kNumBars * 8 + 16 + 1024;  // + 1 KB alignment slack
+  static constexpr int kSmem = kBarOff + kNumBars * 8 + 32 + 1024;  // + 1 KB alignment slack
   static constexpr uint32_t kTmemO = 256;
 };
+
+__device__ __forceinline__ void softmax_bar_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
 
 template <int D, bool kProbe>
 __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_constant__ AttnParams p) {
@@ -101,14 +119,24 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
   uint64_t* p_full = s_full + 2;             // [2]
   uint64_t* o_full = p_full + 2;             // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+  int32_t* last_flag = reinterpret_cast<int32_t*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int rank = blockIdx.x / p.n_qpairs;
-  const int qp = blockIdx.x - rank * p.n_qpairs;
+
+  // ---- work item: (head, query-tile pair, kv piece), heads in LPT order
+  int rank = 0;
+  while (rank + 1 < p.n_heads && p.item_prefix[rank + 1] <= static_cast<int>(blockIdx.x)) ++rank;
   const int h = p.head_order[rank];
   const HeadParam hd = p.heads[h];
-  const int n_kv = (hd.n_tok + kBN - 1) / kBN;
+  const int local = blockIdx.x - p.item_prefix[rank];
+  const int ns = hd.n_split;
+  const int qp = local / ns;
+  const int piece = local - qp * ns;
+  const int n_kv_total = (hd.n_tok + kBN - 1) / kBN;
+  const int kv_begin = (piece * n_kv_total) / ns;
+  const int n_kv = ((piece + 1) * n_kv_total) / ns - kv_begin;
+  const bool two = qp * 2 * kBM + kBM < p.hw;  // second query tile has valid rows
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
@@ -143,16 +171,17 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
       prefetch_tmap(vmap);
       const uint64_t keep = policy_evict_last();  // K/V re-read by every q-tile pair of the head
       const int qrow0 = hd.q_head * p.hw + qp * 2 * kBM;
-      mbar_expect_tx(q_full, 2 * C::kTileBytes);
-      for (int t = 0; t < 2; ++t)
+      const int nq = two ? 2 : 1;
+      mbar_expect_tx(q_full, nq * C::kTileBytes);
+      for (int t = 0; t < nq; ++t)
         for (int b = 0; b < C::kBoxes; ++b)
           tma_load_2d(smem + C::kQOff + t * C::kTileBytes + b * C::kBoxBytes, &p.qmap, q_full, b * 64,
                       qrow0 + t * kBM);
-      for (int j = 0; j < n_kv; ++j) {
-        const int row = hd.base_row + j * kBN;
+      for (int jj = 0; jj < n_kv; ++jj) {
+        const int row = hd.base_row + (kv_begin + jj) * kBN;
         {
-          const int s = j % C::kStagesK;
-          const uint32_t ph = (j / C::kStagesK) & 1;
+          const int s = jj % C::kStagesK;
+          const uint32_t ph = (jj / C::kStagesK) & 1;
           mbar_wait(k_empty + s, ph ^ 1);
           mbar_expect_tx(k_full + s, C::kTileBytes);
           for (int b = 0; b < C::kBoxes; ++b)
@@ -160,8 +189,8 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
                              row, keep);
         }
         {
-          const int s = j % C::kStagesV;
-          const uint32_t ph = (j / C::kStagesV) & 1;
+          const int s = jj % C::kStagesV;
+          const uint32_t ph = (jj / C::kStagesV) & 1;
           mbar_wait(v_empty + s, ph ^ 1);
           mbar_expect_tx(v_full + s, C::kTileBytes);
           for (int b = 0; b < C::kBoxes; ++b)
@@ -206,26 +235,28 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
           umma_ts(tO, tP + kk * 8, sdesc_sw128(vb + kk * 2048, C::kBoxBytes, 1024), idesc_pv,
                   (jj > 0 || kk > 0) ? 1u : 0u);
         umma_commit(o_full + t);
-        if (t == 1) umma_commit(v_empty + vs);
+        if (t == 1 || !two) umma_commit(v_empty + vs);  // last reader of V_jj
       };
 
       mbar_wait(q_full, 0);
       tc_fence_after();
-      for (int j = 0; j < n_kv; ++j) {
-        const int ks = j % C::kStagesK;
-        mbar_wait(k_full + ks, (j / C::kStagesK) & 1);
+      for (int jj = 0; jj < n_kv; ++jj) {
+        const int ks = jj % C::kStagesK;
+        mbar_wait(k_full + ks, (jj / C::kStagesK) & 1);
         tc_fence_after();
         qk(tS0, 0, ks);
         umma_commit(s_full + 0);
-        if (j > 0) pv(1, j - 1);
-        qk(tS1, 1, ks);
-        umma_commit(s_full + 1);
+        if (two) {
+          if (jj > 0) pv(1, jj - 1);
+          qk(tS1, 1, ks);
+          umma_commit(s_full + 1);
+        }
         umma_commit(k_empty + ks);
-        pv(0, j);
+        pv(0, jj);
       }
-      pv(1, n_kv - 1);
+      if (two) pv(1, n_kv - 1);
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && (two || warp < 8)) {
     // ------------------------------------------------------------ softmax
     const int t = (warp - 4) >> 2;        // query tile of this warpgroup
     const int quad = warp & 3;            // TMEM lane quadrant this warp may access
@@ -238,8 +269,9 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
     float l = 0.f;
     float reg_acc[3] = {0.f, 0.f, 0.f};  // probe: sink / neighbor / current mass
 
-    for (int j = 0; j < n_kv; ++j) {
-      mbar_wait(s_full + t, j & 1);
+    for (int jj = 0; jj < n_kv; ++jj) {
+      const int j = kv_begin + jj;
+      mbar_wait(s_full + t, jj & 1);
       tc_fence_after();
       uint32_t r[128];
       tmem_ld32(tS + 0, r + 0);
@@ -263,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
         mx3 = fmaxf(mx3, __uint_as_float(r[c + 3]));
       }
       const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
-      if (j == 0) {
+      if (jj == 0) {
         m = m_tile;
       } else {
         const bool need = m_tile > m + kRescaleThreshold;
@@ -276,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
             reg_acc[1] *= alpha;
             reg_acc[2] *= alpha;
           }
-          mbar_wait(o_full + t, (j - 1) & 1);  // O += P_{j-1} V_{j-1} has landed
+          mbar_wait(o_full + t, (jj - 1) & 1);  // O += P_{jj-1} V_{jj-1} has landed
           tc_fence_after();
 #pragma unroll
           for (int c = 0; c < D / 16; ++c) {
@@ -290,8 +322,9 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
           tmem_wait_st();
         }
       }
-      const float neg_m = -m;
-      float sum0 = 0.f, sum1 = 0.f;
+      const float2 scale2 = make_float2(sl2, sl2);
+      const float2 negm2 = make_float2(-m, -m);
+      float2 sum2 = make_float2(0.f, 0.f);
       float span = 0.f;
       int next_b = 0, kind = 0, slot = 0;
       if constexpr (kProbe) {
@@ -306,10 +339,15 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int c = quarter * 32 + 2 * i;
-          const float a = ex2(fmaf(__uint_as_float(r[c]), sl2, neg_m));
-          const float b = ex2(fmaf(__uint_as_float(r[c + 1]), sl2, neg_m));
-          sum0 += a;
-          sum1 += b;
+          const float2 x = fma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
+          float2 e;
+          if ((c / 2) % kEmuEvery == kEmuEvery - 1) {  // compile-time: every kEmuEvery-th pair on the FMA pipe
+            e = exp2_poly2(x);
+          } else {
+            e = make_float2(ex2(x.x), ex2(x.y));
+          }
+          const float a = e.x, b = e.y;
+          sum2 = add2(sum2, e);
           pk[i] = pack_bf16x2(a, b);
           if constexpr (kProbe) {
 #pragma unroll
@@ -334,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
         reg_acc[1] += kind == 1 ? span : 0.f;
         reg_acc[2] += kind == 2 ? span : 0.f;
       }
-      l += sum0 + sum1;
+      l += sum2.x + sum2.y;
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(p_full + t);
@@ -343,36 +381,101 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
     // ------------------------------------------------------------ epilogue
     mbar_wait(o_full + t, (n_kv - 1) & 1);
     tc_fence_after();
-    const int row = qp * 2 * kBM + t * kBM + row_local;
+    const int prow = t * kBM + row_local;           // row within the pair
+    const int row = qp * 2 * kBM + prow;            // row within the head
     const bool row_ok = row < p.hw;
-    const float inv_l = 1.f / l;
     __nv_bfloat16* orow = p.out + (static_cast<int64_t>(hd.o_head) * p.hw + row) * p.out_ld;
+    auto store_row = [&](const float* o, int c0, float scale) {
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t o[32];
-      tmem_ld32(tO + c * 32, o);
-      tmem_wait_ld();
-      if (row_ok) {
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int col = c * 32 + v * 8;
-          if (col < p.d_out) {
-            uint4 w;
-            w.x = pack_bf16x2(__uint_as_float(o[v * 8 + 0]) * inv_l, __uint_as_float(o[v * 8 + 1]) * inv_l);
-            w.y = pack_bf16x2(__uint_as_float(o[v * 8 + 2]) * inv_l, __uint_as_float(o[v * 8 + 3]) * inv_l);
-            w.z = pack_bf16x2(__uint_as_float(o[v * 8 + 4]) * inv_l, __uint_as_float(o[v * 8 + 5]) * inv_l);
-            w.w = pack_bf16x2(__uint_as_float(o[v * 8 + 6]) * inv_l, __uint_as_float(o[v * 8 + 7]) * inv_l);
-            *reinterpret_cast<uint4*>(orow + col) = w;
-          }
+      for (int v = 0; v < 4; ++v) {
+        const int col = c0 + v * 8;
+        if (col < p.d_out) {
+          uint4 w;
+          w.x = pack_bf16x2(o[v * 8 + 0] * scale, o[v * 8 + 1] * scale);
+          w.y = pack_bf16x2(o[v * 8 + 2] * scale, o[v * 8 + 3] * scale);
+          w.z = pack_bf16x2(o[v * 8 + 4] * scale, o[v * 8 + 5] * scale);
+          w.w = pack_bf16x2(o[v * 8 + 6] * scale, o[v * 8 + 7] * scale);
+          *reinterpret_cast<uint4*>(orow + col) = w;
         }
       }
-    }
-    if constexpr (kProbe) {
-      if (row_ok && p.row_sampled[row]) {
-        float* dst = p.probe_rows + (static_cast<int64_t>(h) * p.hw + row) * 3;
-        dst[0] = reg_acc[0] * inv_l;
-        dst[1] = reg_acc[1] * inv_l;
-        dst[2] = reg_acc[2] * inv_l;
+    };
+    if (ns == 1) {
+      const float inv_l = 1.f / l;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t o[32];
+        tmem_ld32(tO + c * 32, o);
+        tmem_wait_ld();
+        if (row_ok) store_row(reinterpret_cast<const float*>(o), c * 32, inv_l);
+      }
+      if constexpr (kProbe) {
+        if (row_ok && p.row_sampled[row]) {
+          float* dst = p.probe_rows + (static_cast<int64_t>(h) * p.hw + row) * 3;
+          dst[0] = reg_acc[0] * inv_l;
+          dst[1] = reg_acc[1] * inv_l;
+          dst[2] = reg_acc[2] * inv_l;
+        }
+      }
+    } else {
+      // split-KV: publish this piece's (O, m, l); the last piece of the pair combines.
+      const int group = hd.group_base + qp;
+      const int64_t slot0 = static_cast<int64_t>(hd.part_base) + static_cast<int64_t>(qp) * ns;
+      float* my_o = p.ws_o + ((slot0 + piece) * 2 * kBM + prow) * D;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t o[32];
+        tmem_ld32(tO + c * 32, o);
+        tmem_wait_ld();
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          __stcg(reinterpret_cast<float4*>(my_o + c * 32 + v * 4),
+                 make_float4(__uint_as_float(o[4 * v]), __uint_as_float(o[4 * v + 1]), __uint_as_float(o[4 * v + 2]),
+                             __uint_as_float(o[4 * v + 3])));
+      }
+      __stcg(reinterpret_cast<float2*>(p.ws_ml + ((slot0 + piece) * 2 * kBM + prow) * 2), make_float2(m, l));
+      __threadfence();
+      const int nthreads = two ? 256 : 128;
+      softmax_bar_sync(nthreads);
+      if (threadIdx.x == 128) {
+        const int prev = atomicAdd(p.ws_cnt + group, 1);
+        *last_flag = (prev == ns - 1);
+        if (prev == ns - 1) p.ws_cnt[group] = 0;  // ready for the next launch
+        __threadfence();
+      }
+      softmax_bar_sync(nthreads);
+      if (*last_flag && row_ok) {
+        float mi[16], li[16];
+        float M = -INFINITY;
+        for (int i = 0; i < ns; ++i) {
+          const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((slot0 + i) * 2 * kBM + prow) * 2));
+          mi[i] = ml.x;
+          li[i] = ml.y;
+          M = fmaxf(M, ml.x);
+        }
+        float den = 0.f;
+        for (int i = 0; i < ns; ++i) {
+          mi[i] = ex2(mi[i] - M);
+          den += mi[i] * li[i];
+        }
+        const float inv = 1.f / den;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          float acc[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) acc[e] = 0.f;
+          for (int i = 0; i < ns; ++i) {
+            const float* src = p.ws_o + ((slot0 + i) * 2 * kBM + prow) * D + c * 32;
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              const float4 x = __ldcg(reinterpret_cast<const float4*>(src + v * 4));
+              acc[4 * v + 0] += mi[i] * x.x;
+              acc[4 * v + 1] += mi[i] * x.y;
+              acc[4 * v + 2] += mi[i] * x.z;
+              acc[4 * v + 3] += mi[i] * x.w;
+            }
+          }
+          store_row(acc, c * 32, inv);
+        }
       }
     }
   }
@@ -405,7 +508,149 @@ static int launch_attn(const AttnParams& p, int grid, cudaStream_t stream) {
 
 using namespace dfb;
 
-extern "C" int df_attn_fwd(const df_attn_args* a, void* stream) {
+namespace {
+
+// ------------------------------------------------------------------ planner
+// Hardware list-schedules CTAs in blockIdx order as SMs free up, so the
+// launch order below (heads by decreasing piece cost, pairs ascending) is LPT.
+// The planner picks per-head kv split counts that minimise the simulated
+// makespan over the SMs, charging a fixed prologue/epilogue cost per CTA and
+// a combine cost per split piece.  Cost unit: one 128-key tile for a full
+// pair of 128-row query tiles.
+constexpr double kPieceOverhead = 3.0;
+constexpr double kSplitOverhead = 2.0;
+constexpr double kSingleTileFactor = 0.6;  // last pair with only its first tile valid
+constexpr int kMaxSplit = 16;
+
+struct Plan {
+  uint8_t ns[DF_MAX_HEADS];
+  int order[DF_MAX_HEADS];
+  int64_t ws_bytes;
+  int n_items;
+};
+
+int sm_count_cached() {
+  static int count = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev);
+    if (count <= 0) count = 148;
+  });
+  return count;
+}
+
+double simulate(const df_attn_args* a, const uint8_t* ns, const int* order, int sms) {
+  const int nq = (a->hw + 255) / 256;
+  const bool last_single = (nq - 1) * 256 + 128 >= a->hw;
+  std::priority_queue<double, std::vector<double>, std::greater<double>> bins;
+  for (int i = 0; i < sms; ++i) bins.push(0.0);
+  double makespan = 0.0;
+  for (int r = 0; r < a->num_heads; ++r) {
+    const int h = order[r];
+    const int tiles = (a->heads[h].n_tok + 127) / 128;
+    for (int qp = 0; qp < nq; ++qp) {
+      const double f = (qp == nq - 1 && last_single) ? kSingleTileFactor : 1.0;
+      for (int s = 0; s < ns[h]; ++s) {
+        const int len = ((s + 1) * tiles) / ns[h] - (s * tiles) / ns[h];
+        const double c = len * f + kPieceOverhead + (ns[h] > 1 ? kSplitOverhead : 0.0);
+        const double t0 = bins.top();
+        bins.pop();
+        bins.push(t0 + c);
+        makespan = std::max(makespan, t0 + c);
+      }
+    }
+  }
+  return makespan;
+}
+
+void order_heads(const df_attn_args* a, const uint8_t* ns, int* order) {
+  for (int i = 0; i < a->num_heads; ++i) order[i] = i;
+  std::stable_sort(order, order + a->num_heads, [&](int x, int y) {
+    const double cx = double((a->heads[x].n_tok + 127) / 128) / ns[x];
+    const double cy = double((a->heads[y].n_tok + 127) / 128) / ns[y];
+    return cx > cy;
+  });
+}
+
+int64_t workspace_need(const df_attn_args* a, const uint8_t* ns) {
+  const int nq = (a->hw + 255) / 256;
+  int64_t groups = 0, slots = 0;
+  for (int h = 0; h < a->num_heads; ++h)
+    if (ns[h] > 1) {
+      groups += nq;
+      slots += int64_t(nq) * ns[h];
+    }
+  if (!groups) return 0;
+  const int64_t cnt_bytes = ((groups * 4 + 255) / 256) * 256;
+  return cnt_bytes + slots * 256 * (int64_t(a->head_dim) + 2) * 4;
+}
+
+Plan make_plan(const df_attn_args* a, bool allow_split) {
+  Plan best{};
+  const int sms = sm_count_cached();
+  for (int i = 0; i < a->num_heads; ++i) best.ns[i] = 1;
+  order_heads(a, best.ns, best.order);
+  double best_t = simulate(a, best.ns, best.order, sms);
+  if (allow_split) {
+    int max_tiles = 1;
+    for (int h = 0; h < a->num_heads; ++h) max_tiles = std::max(max_tiles, (a->heads[h].n_tok + 127) / 128);
+    // candidate caps on tiles per piece
+    for (int cap = 8; cap < max_tiles; cap += std::max(1, cap / 8)) {
+      Plan c{};
+      for (int h = 0; h < a->num_heads; ++h) {
+        const int tiles = (a->heads[h].n_tok + 127) / 128;
+        c.ns[h] = static_cast<uint8_t>(std::min(kMaxSplit, std::max(1, (tiles + cap - 1) / cap)));
+      }
+      order_heads(a, c.ns, c.order);
+      const double t = simulate(a, c.ns, c.order, sms);
+      if (t < best_t * 0.995) {
+        best_t = t;
+        std::memcpy(best.ns, c.ns, sizeof(c.ns));
+        std::memcpy(best.order, c.order, sizeof(c.order));
+      }
+    }
+  }
+  best.ws_bytes = workspace_need(a, best.ns);
+  const int nq = (a->hw + 255) / 256;
+  best.n_items = 0;
+  for (int h = 0; h < a->num_heads; ++h) best.n_items += nq * best.ns[h];
+  return best;
+}
+
+// Plans are cached per (hw, head_dim, n_tok list, probe) -- a session issues
+// the same signature for every layer of a step.
+struct PlanCache {
+  std::mutex mu;
+  std::map<std::vector<int64_t>, Plan> map;
+};
+PlanCache& plan_cache() {
+  static PlanCache c;
+  return c;
+}
+
+Plan get_plan(const df_attn_args* a, bool allow_split) {
+  std::vector<int64_t> key;
+  key.reserve(a->num_heads + 4);
+  key.push_back(a->hw);
+  key.push_back(a->head_dim);
+  key.push_back(allow_split);
+  key.push_back(sm_count_cached());
+  for (int i = 0; i < a->num_heads; ++i) key.push_back(a->heads[i].n_tok);
+  PlanCache& pc = plan_cache();
+  {
+    std::lock_guard<std::mutex> g(pc.mu);
+    auto it = pc.map.find(key);
+    if (it != pc.map.end()) return it->second;
+  }
+  Plan p = make_plan(a, allow_split);
+  std::lock_guard<std::mutex> g(pc.mu);
+  if (pc.map.size() > 4096) pc.map.clear();
+  pc.map.emplace(std::move(key), p);
+  return p;
+}
+
+int validate(const df_attn_args* a) {
   if (!a) return set_error(DF_E_ARG, "df_attn_fwd: null args");
   if (a->head_dim != 64 && a->head_dim != 128)
     return set_error(DF_E_SHAPE, "df_attn_fwd: head_dim must be 64 or 128 (got %d)", a->head_dim);
@@ -421,13 +666,46 @@ extern "C" int df_attn_fwd(const df_attn_args* a, void* stream) {
   if (a->q_rows < 1 || a->q_rows > INT32_MAX) return set_error(DF_E_SHAPE, "df_attn_fwd: bad q_rows");
   if ((reinterpret_cast<uintptr_t>(a->q) & 15) || (reinterpret_cast<uintptr_t>(a->out) & 15) || (a->out_ld % 8))
     return set_error(DF_E_ARG, "df_attn_fwd: q/out must be 16-byte aligned, out_ld a multiple of 8");
+  for (int i = 0; i < a->num_heads; ++i) {
+    const df_head_desc& h = a->heads[i];
+    if (h.n_tok < 1) return set_error(DF_E_SHAPE, "df_attn_fwd: head %d has empty context", i);
+    if (h.arena < 0 || h.arena >= a->num_arenas) return set_error(DF_E_ARG, "df_attn_fwd: head %d bad arena", i);
+    if (h.base_row < 0 || h.base_row + h.n_tok > INT32_MAX)
+      return set_error(DF_E_ARG, "df_attn_fwd: head %d arena rows out of int32 range", i);
+    if (h.q_head < 0 || static_cast<int64_t>(h.q_head) * a->hw >= a->q_rows || h.o_head < 0 || h.q_head > 32767 ||
+        h.o_head > 32767)
+      return set_error(DF_E_SHAPE, "df_attn_fwd: head %d q/o index out of range", i);
+  }
+  return DF_OK;
+}
+
+}  // namespace
+
+extern "C" int df_attn_workspace_bytes(const df_attn_args* a, int64_t* bytes) {
+  int rc = validate(a);
+  if (rc != DF_OK) return rc;
+  if (!bytes) return set_error(DF_E_ARG, "df_attn_workspace_bytes: null output");
+  const bool probe = (a->flags & DF_ATTN_PROBE) != 0;
+  *bytes = get_plan(a, !probe).ws_bytes;
+  return DF_OK;
+}
+
+extern "C" int df_attn_fwd(const df_attn_args* a, void* stream) {
+  int rc = validate(a);
+  if (rc != DF_OK) return rc;
   const bool probe = (a->flags & DF_ATTN_PROBE) != 0;
   if (probe && (!a->region_of_slot || !a->row_sampled || !a->probe_rows || a->max_slots < 1))
     return set_error(DF_E_ARG, "df_attn_fwd: probe epilogue needs region_of_slot, row_sampled, probe_rows");
 
+  // Split plan; fall back to no splitting when the workspace cannot hold it.
+  Plan plan = get_plan(a, !probe);
+  if (plan.ws_bytes > 0 && (!a->workspace || a->workspace_bytes < plan.ws_bytes ||
+                            (reinterpret_cast<uintptr_t>(a->workspace) & 255)))
+    plan = get_plan(a, false);
+
   AttnParams p;
   std::memset(&p, 0, sizeof(p));
-  int rc = encode_rowmajor_bf16(&p.qmap, a->q, a->q_rows, a->head_dim);
+  rc = encode_rowmajor_bf16(&p.qmap, a->q, a->q_rows, a->head_dim);
   if (rc != DF_OK) return rc;
   std::memcpy(p.kvmap, a->kv_maps, static_cast<size_t>(a->num_arenas) * 2 * DF_TMAP_BYTES);
   p.out = static_cast<__nv_bfloat16*>(a->out);
@@ -442,30 +720,39 @@ extern "C" int df_attn_fwd(const df_attn_args* a, void* stream) {
   p.probe_rows = a->probe_rows;
   p.scale_log2 = a->scale * 1.4426950408889634f;
 
-  int order[DF_MAX_HEADS];
+  int64_t groups = 0, slots = 0;
   for (int i = 0; i < a->num_heads; ++i) {
     const df_head_desc& h = a->heads[i];
-    if (h.n_tok < 1) return set_error(DF_E_SHAPE, "df_attn_fwd: head %d has empty context", i);
-    if (h.arena < 0 || h.arena >= a->num_arenas) return set_error(DF_E_ARG, "df_attn_fwd: head %d bad arena", i);
-    if (h.base_row < 0 || h.base_row + h.n_tok > INT32_MAX)
-      return set_error(DF_E_ARG, "df_attn_fwd: head %d arena rows out of int32 range", i);
-    if (h.q_head < 0 || static_cast<int64_t>(h.q_head) * a->hw >= a->q_rows || h.o_head < 0 || h.q_head > 32767 ||
-        h.o_head > 32767)
-      return set_error(DF_E_SHAPE, "df_attn_fwd: head %d q/o index out of range", i);
-    p.heads[i].base_row = static_cast<int32_t>(h.base_row);
-    p.heads[i].n_tok = h.n_tok;
-    p.heads[i].q_head = static_cast<int16_t>(h.q_head);
-    p.heads[i].o_head = static_cast<int16_t>(h.o_head);
-    p.heads[i].arena = static_cast<int16_t>(h.arena);
-    order[i] = i;
+    HeadParam& hp = p.heads[i];
+    hp.base_row = static_cast<int32_t>(h.base_row);
+    hp.n_tok = h.n_tok;
+    hp.q_head = static_cast<int16_t>(h.q_head);
+    hp.o_head = static_cast<int16_t>(h.o_head);
+    hp.arena = static_cast<int16_t>(h.arena);
+    hp.n_split = plan.ns[i];
+    if (plan.ns[i] > 1) {
+      hp.group_base = static_cast<int32_t>(groups);
+      hp.part_base = static_cast<int32_t>(slots);
+      groups += p.n_qpairs;
+      slots += int64_t(p.n_qpairs) * plan.ns[i];
+    }
   }
-  // Longest context first: the block scheduler then issues the heaviest work
-  // items first (LPT), keeping the tail short when heads are heterogeneous.
-  std::stable_sort(order, order + a->num_heads,
-                   [&](int x, int y) { return a->heads[x].n_tok > a->heads[y].n_tok; });
-  for (int i = 0; i < a->num_heads; ++i) p.head_order[i] = static_cast<uint8_t>(order[i]);
+  if (groups) {
+    const int64_t cnt_bytes = ((groups * 4 + 255) / 256) * 256;
+    uint8_t* ws = static_cast<uint8_t*>(a->workspace);
+    p.ws_cnt = reinterpret_cast<int32_t*>(ws);
+    p.ws_o = reinterpret_cast<float*>(ws + cnt_bytes);
+    p.ws_ml = p.ws_o + slots * 2 * kBM * a->head_dim;
+  }
+  int acc = 0;
+  for (int r = 0; r < a->num_heads; ++r) {
+    p.head_order[r] = static_cast<uint8_t>(plan.order[r]);
+    p.item_prefix[r] = acc;
+    acc += p.n_qpairs * plan.ns[plan.order[r]];
+  }
+  p.item_prefix[a->num_heads] = acc;
 
-  const int grid = a->num_heads * p.n_qpairs;
+  const int grid = acc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (a->head_dim == 128)
     return probe ? launch_attn<128, true>(p, grid, s) : launch_attn<128, false>(p, grid, s);

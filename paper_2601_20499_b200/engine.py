@@ -413,12 +413,9 @@ class Session:
         rows = sum(K.KVArena.region_rows(p.ring_slots * cfg.HW) for p in policies)
         arena = K.KVArena(rows, K.padded_width(cfg.head_dim), self.device)
         s = self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        new = rebuild_caches(flat_caches, policies, arena, stream=s)
-        e1.record(s)
-        moved = sum(len(c) for c in new) * cfg.HW * arena.width * 2 * 2 * 2  # K+V, read+write
-        self.pack_stats = {"bytes": moved, "events": (e0, e1)}
+        stats: dict = {}
+        new = rebuild_caches(flat_caches, policies, arena, stream=s, stats=stats)
+        self.pack_stats = stats
         H = cfg.num_heads
         self.caches = [new[l * H : (l + 1) * H] for l in range(cfg.num_layers)]
 

@@ -16,6 +16,7 @@ from . import _lib
 from .errors import ShapeError
 
 TOKEN_ALIGN = 128  # head regions start on a kv-tile boundary
+SPLIT_KV = True  # provide a split-KV workspace (the C planner decides whether to split)
 SUPPORTED_WIDTHS = (64, 128)
 
 
@@ -186,7 +187,31 @@ def attention(
         args.region_of_slot = probe.region_of_slot.data_ptr()
         args.row_sampled = probe.row_sampled.data_ptr()
         args.probe_rows = probe.probe_rows.data_ptr()
-    _lib.call("df_attn_fwd", ctypes.byref(args), _stream_handle(stream))
+    handle = _stream_handle(stream)
+    need = ctypes.c_int64(0)
+    _lib.call("df_attn_workspace_bytes", ctypes.byref(args), ctypes.byref(need))
+    if need.value > 0 and SPLIT_KV:
+        ws = _split_workspace(q.device, handle.value, need.value)
+        args.workspace = ws.data_ptr()
+        args.workspace_bytes = ws.numel()
+    _lib.call("df_attn_fwd", ctypes.byref(args), handle)
+
+
+_WORKSPACES: dict[tuple[int, int], torch.Tensor] = {}
+
+
+def _split_workspace(device: torch.device, stream_handle: int, nbytes: int) -> torch.Tensor:
+    """Per-(device, stream) split-KV workspace, zero-filled at allocation.
+
+    The kernel returns every combine counter to zero, so the buffer can be
+    reused by the next launch on the same stream without a memset.
+    """
+    key = (device.index if device.index is not None else torch.cuda.current_device(), stream_handle or 0)
+    ws = _WORKSPACES.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        _WORKSPACES[key] = ws
+    return ws
 
 
 def copy_segments(segs: list[tuple[int, int, int, int, int, int]], stream: torch.cuda.Stream | None = None) -> None:

@@ -353,7 +353,7 @@ def _same_staging(staged, block: FrameBlock, slot: int, arena) -> bool:
 
 
 def rebuild_caches(caches: list[HeadKVCache], policies: list[CachePolicy], arena: K.KVArena | None = None,
-                   stream=None) -> list[HeadKVCache]:
+                   stream=None, stats: dict | None = None) -> list[HeadKVCache]:
     """Re-lay many heads' retained frames under new policies: ONE df_kv_pack launch.
 
     The new rings live in ``arena`` (allocated here if None).  Retention is
@@ -395,7 +395,15 @@ def rebuild_caches(caches: list[HeadKVCache], policies: list[CachePolicy], arena
         out.append(n)
     if segs:
         plan = K.PackPlan(segs, arena.device)
-        plan.launch(stream)
+        if stats is not None:  # device time of the df_kv_pack launch alone
+            s = stream if stream is not None else torch.cuda.current_stream(arena.device)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record(s)
+            plan.launch(s)
+            ev[1].record(s)
+            stats.update(bytes=plan.bytes_moved, events=tuple(ev), blocks=plan.total_blocks)
+        else:
+            plan.launch(stream)
     return out
 
 

@@ -17,6 +17,9 @@ def _ref(q, k, v, scale):
     (128, 300, [300, 600, 1000]),
     (64, 192, [192, 384, 1344, 576]),
     (128, 4680, [9360, 4680 * 7]),
+    (128, 600, [131072]),            # one long head: planner splits kv, in-kernel combine
+    (64, 300, [40000, 300, 900]),    # split + unsplit heads in one launch, ragged tails
+    (128, 200, [2000] * 40),         # many heads; last pair has a single valid tile
 ])
 def test_attention_matches_torch(width, hw, ctxs):
     from paper_2601_20499_b200 import kernels as K
