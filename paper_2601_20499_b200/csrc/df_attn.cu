@@ -47,7 +47,7 @@ constexpr int kWarps = 12;  // see role map above
 constexpr int kThreads = kWarps * 32;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 #ifndef DF_EMU_EVERY
-#define DF_EMU_EVERY 4
+#define DF_EMU_EVERY 8
 #endif
 constexpr int kEmuEvery = DF_EMU_EVERY;  // 1 in kEmuEvery exp2 pairs runs as a polynomial on the FMA pipe
 
@@ -95,7 +95,7 @@ struct AttnCfg {
   static constexpr int kKOff = kQOff + 2 * kTileBytes;
   static constexpr int kVOff = kKOff + kStagesK * kTileBytes;
   static constexpr int kBarOff = kVOff + kStagesV * kTileBytes;
-  static constexpr int kNumBars = 1 + 2 * kStagesK + 2 * kStagesV + 6;
+  static constexpr int kNumBars = 1 + 2 * kStagesK + 2 * kStagesV + 8;
   static constexpr int kSmem = kBarOff + kNumBars * 8 + 32 + 1024;  // + 1 KB alignment slack
   static constexpr uint32_t kTmemO = 256;
 };
@@ -116,8 +116,8 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
   uint64_t* v_full = k_empty + C::kStagesK;
   uint64_t* v_empty = v_full + C::kStagesV;
   uint64_t* s_full = v_empty + C::kStagesV;  // [2]
-  uint64_t* p_full = s_full + 2;             // [2]
-  uint64_t* o_full = p_full + 2;             // [2]
+  uint64_t* p_full = s_full + 2;             // [2 tiles][2 halves of P]
+  uint64_t* o_full = p_full + 4;             // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
   int32_t* last_flag = reinterpret_cast<int32_t*>(tmem_slot + 1);
 
@@ -150,7 +150,8 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(s_full + t, 1);
-      mbar_init(p_full + t, 128);
+      mbar_init(p_full + 2 * t, 128);
+      mbar_init(p_full + 2 * t + 1, 128);
       mbar_init(o_full + t, 1);
     }
     fence_mbar_init();
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
       };
       auto pv = [&](int t, int jj) {
         const int vs = jj % C::kStagesV;
-        mbar_wait(p_full + t, jj & 1);
+        mbar_wait(p_full + 2 * t, jj & 1);  // first half of P (keys 0-63) is in TMEM
         tc_fence_after();
         if (t == 0) {
           mbar_wait(v_full + vs, (jj / C::kStagesV) & 1);
@@ -231,9 +232,14 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
         const uint32_t tP = t ? tS1 : tS0;
         const uint32_t tO = t ? tO1 : tO0;
 #pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk)
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          if (kk == kBN / 32) {  // second half of P (keys 64-127)
+            mbar_wait(p_full + 2 * t + 1, jj & 1);
+            tc_fence_after();
+          }
           umma_ts(tO, tP + kk * 8, sdesc_sw128(vb + kk * 2048, C::kBoxBytes, 1024), idesc_pv,
                   (jj > 0 || kk > 0) ? 1u : 0u);
+        }
         umma_commit(o_full + t);
         if (t == 1 || !two) umma_commit(v_empty + vs);  // last reader of V_jj
       };
@@ -366,6 +372,11 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
           }
         }
         tmem_st16(tS + quarter * 16, pk);
+        if (quarter == 1) {  // release the first half of P early: PV can start on keys 0-63
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(p_full + 2 * t);
+        }
       }
       if constexpr (kProbe) {
         reg_acc[0] += kind == 0 ? span : 0.f;
@@ -375,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
       l += sum2.x + sum2.y;
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(p_full + t);
+      mbar_arrive(p_full + 2 * t + 1);
     }
 
     // ------------------------------------------------------------ epilogue

@@ -204,11 +204,12 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) {
 // 2^x on the FMA pipe (offloads MUFU, which co-limits attention at d=128):
 // x = j + f with j = rint(x) (magic-number rounding), 2^f by a degree-3
 // minimax polynomial on [-0.5, 0.5] (max rel err 7.5e-5, far below the bf16
-// rounding of P), 2^j added into the exponent field.  x is clamped at -127 so
-// masked (-inf) columns give ~6e-39 instead of exactly 0.
+// rounding of P), 2^j added into the exponent field.  x is clamped at -126 (a
+// result < 1 has exponent 126, so j >= -126 keeps the sum >= 0): masked (-inf)
+// columns give ~1e-38 instead of exactly 0 (tests/test_gpu_attn_kernel.py).
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -127.f);
-  x.y = fmaxf(x.y, -127.f);
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
   const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
   const float2 t = add2(x, magic);
   const float2 j = add2(t, make_float2(-12582912.f, -12582912.f));

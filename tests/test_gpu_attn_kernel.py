@@ -46,3 +46,30 @@ def test_attention_matches_torch(width, hw, ctxs):
         got = out[h * hw:(h + 1) * hw].float()
         err = (got - ref).abs().max().item() / ref.abs().max().item()
         assert err <= 2e-2, (h, err)
+
+
+@pytest.mark.parametrize("scale_q", [1.0, 6.0])
+def test_stale_rows_and_masked_tails(scale_q):
+    """Arena rows past each head's context hold stale finite data (as after an
+    eviction): masked tail columns must contribute nothing, with both the MUFU
+    and the polynomial exp2 paths; large logits exercise the lazy rescale."""
+    from paper_2601_20499_b200 import kernels as K
+
+    torch.manual_seed(1)
+    dev = torch.device("cuda:0")
+    hw, width, ctxs = 300, 128, [300, 600, 1000, 4680 * 2 + 77]
+    arena = K.KVArena(sum(K.KVArena.region_rows(c) for c in ctxs), width, dev)
+    arena.k.normal_()
+    arena.v.normal_()
+    q = (torch.randn(len(ctxs) * hw, width, device=dev) * scale_q).to(torch.bfloat16)
+    out = torch.full((len(ctxs) * hw, width), float("nan"), device=dev, dtype=torch.bfloat16)
+    work = [K.HeadWork(arena, arena.allocate(c), c, h, h) for h, c in enumerate(ctxs)]
+    scale = 1.0 / math.sqrt(width)
+    K.attention(q, out, work, hw, scale)
+    torch.cuda.synchronize()
+    assert not torch.isnan(out.float()).any()
+    for h, w in enumerate(work):
+        ref = _ref(q[h * hw:(h + 1) * hw], arena.k[w.base_row:w.base_row + w.n_tok],
+                   arena.v[w.base_row:w.base_row + w.n_tok], scale)
+        err = (out[h * hw:(h + 1) * hw].float() - ref).abs().max().item() / ref.abs().max().item()
+        assert err <= 2e-2, (h, err)
