@@ -63,6 +63,21 @@ PACKED_CTX = [2 * HW] * 6 + [2 * HW] * 3 + [6 * HW] * 3  # dummy [i-1,i], sink [
 BASE_CTX = [7 * HW] * 12
 
 
+def ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum of one packed launch from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "r1_attn_packed_ncu.json")
+    if not os.path.exists(p):
+        return None
+    j = json.load(open(p))
+    mb = float(j["dram__bytes_read.sum"]["value"]) + float(j["dram__bytes_write.sum"]["value"])
+    return int(mb * 1e6)
+
+
+def attn_alg_bytes():
+    """Q + K/V of every head once + O (packed layer)."""
+    return (H * HW * D * 2) * 2 + sum(PACKED_CTX) * D * 2 * 2
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
@@ -342,7 +357,9 @@ def gpu_arm(args, ws, rank, local):
                                  "tflops_step": flops_base * L / (t_base * 1e-3) / 1e12,
                                  "speedup_packed_vs_all_context": t_base / t_step},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
-                     "frac": achieved / bf16_peak, "traffic": None, "kernel": "df_attn_kernel<128,false>",
+                     "frac": achieved / bf16_peak, "traffic": ncu_traffic(),
+                     "traffic_unit": "bytes per launch (dram read+write, profiles/r1_attn_packed_ncu.json)",
+                     "algorithmic_bytes": attn_alg_bytes(), "kernel": "df_attn_kernel<128,false>",
                      "flops_per_launch": flops_packed, "peak_source": peak_kind},
         "pack_roofline": {"bound": "hbm", "achieved": pack_gbs, "peak": hbm_peak, "unit": "GB/s",
                           "frac": pack_gbs / hbm_peak, "bytes": pack_bytes, "ms": min(pack_ms),

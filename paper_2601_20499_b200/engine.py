@@ -329,6 +329,9 @@ class Session:
         self.model = model
         self.config = config
         self.mode = mode
+        # heads this process owns ([h0, h1) of every layer); head-parallel
+        # subclasses narrow it and override the three collective hooks below.
+        self.head_range = self._owned_heads()
         self.observer = observer
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.stream = stream
@@ -350,14 +353,27 @@ class Session:
         self._shadow = shadow and mode != "baseline"
         self.shadow_caches = self._fresh_caches() if self._shadow else None
 
+    def _owned_heads(self) -> range:
+        return range(self.config.num_heads)
+
+    # collective hooks (identity on one process; see parallel.HeadParallelSession)
+    def _gather_outputs(self, layer: int, outputs: torch.Tensor) -> torch.Tensor:
+        """Local heads' outputs (h_local, HW, d) -> all heads, for ``mix``."""
+        return outputs
+
+    def _gather_scores(self, local: torch.Tensor) -> torch.Tensor:
+        """(layers, h_local, 3) probe scores -> (layers, heads, 3) on every process."""
+        return local
+
     def _fresh_caches(self) -> list[list[HeadKVCache]]:
         cfg = self.config
         pol = baseline_policy(cfg)
         per = K.KVArena.region_rows(pol.ring_slots * cfg.HW)
-        arena = K.KVArena(per * cfg.total_heads, K.padded_width(cfg.head_dim), self.device)
+        nh = len(self.head_range)
+        arena = K.KVArena(per * cfg.num_layers * nh, K.padded_width(cfg.head_dim), self.device)
         return [[HeadKVCache(pol, storage=RingStorage(arena, arena.allocate(pol.ring_slots * cfg.HW), pol.ring_slots,
                                                       cfg.HW, cfg.head_dim))
-                 for _ in range(cfg.num_heads)] for _ in range(cfg.num_layers)]
+                 for _ in range(nh)] for _ in range(cfg.num_layers)]
 
     # ------------------------------------------------------------ probe
     def _probe_key(self, probe: Probe | None) -> tuple[int, int]:
@@ -391,7 +407,8 @@ class Session:
 
     def _classes_for_layer(self, layer: int) -> list[HeadClass]:
         h = self.config.num_heads
-        return list(self.assignment.classes[layer * h : (layer + 1) * h])
+        r = self.head_range
+        return list(self.assignment.classes[layer * h + r.start : layer * h + r.stop])
 
     def _layer_attention(self, layer, q, caches, current_blocks, probe=None):
         mode = self._effective_mode()
@@ -409,14 +426,15 @@ class Session:
         self.assignment, self.objective = greedy_classify(table, cfg.dummy_count)
         ext = extension_window(self.assignment, cfg) if cfg.context_extension else None
         flat_caches = [c for layer in self.caches for c in layer]
-        policies = [derive_policy(c, cfg, extended_window=ext) for c in self.assignment.classes]
+        policies = [derive_policy(c, cfg, extended_window=ext)
+                    for layer in range(cfg.num_layers) for c in self._classes_for_layer(layer)]
         rows = sum(K.KVArena.region_rows(p.ring_slots * cfg.HW) for p in policies)
         arena = K.KVArena(rows, K.padded_width(cfg.head_dim), self.device)
         s = self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
         stats: dict = {}
         new = rebuild_caches(flat_caches, policies, arena, stream=s, stats=stats)
         self.pack_stats = stats
-        H = cfg.num_heads
+        H = len(self.head_range)
         self.caches = [new[l * H : (l + 1) * H] for l in range(cfg.num_layers)]
 
     def _probe_buffers(self, ratio: float) -> ProbeRequest:
@@ -424,7 +442,7 @@ class Session:
         rows = subsample_rows(cfg.HW, ratio)
         flags = torch.zeros(cfg.HW, dtype=torch.uint8)
         flags[torch.from_numpy(rows)] = 1
-        return ProbeRequest(flags.to(self.device), torch.zeros(cfg.num_heads, cfg.HW, 3, dtype=torch.float32,
+        return ProbeRequest(flags.to(self.device), torch.zeros(len(self.head_range), cfg.HW, 3, dtype=torch.float32,
                                                                 device=self.device))
 
     def _finalize_probe(self, key, ratio, per_layer: list[ProbeRequest]) -> None:
@@ -432,10 +450,14 @@ class Session:
         for pr in per_layer:
             F = K.scores_finalize(K.ProbeBuffers(None, pr.row_sampled, pr.probe_rows), self.stream)
             tables.append(F)
-        self._probe_tables[(key[0], key[1], ratio)] = torch.cat(tables).cpu().numpy()
+        full = self._gather_scores(torch.stack(tables))  # (layers, heads, 3), layer-major flat order
+        self._probe_tables[(key[0], key[1], ratio)] = full.reshape(-1, 3).cpu().numpy()
 
     def _model_qkv(self, layer, x, ar, t):
         q, k, v = self.model.qkv(layer, x, ar, t)
+        r = self.head_range
+        if len(r) != self.config.num_heads:
+            q, k, v = q[r.start : r.stop], k[r.start : r.stop], v[r.start : r.stop]
         return as_device_bf16(q, self.device), as_device_bf16(k, self.device), as_device_bf16(v, self.device)
 
     def _run_step(self, ar_step: int) -> None:
@@ -451,7 +473,7 @@ class Session:
             counters = StepCounters()
             for layer in range(cfg.num_layers):
                 q, k, v = self._model_qkv(layer, x, ar_step, t)
-                blocks = [FrameBlock(ar_step, k[h], v[h]) for h in range(cfg.num_heads)]
+                blocks = [FrameBlock(ar_step, k[h], v[h]) for h in range(k.shape[0])]
                 pr = None
                 if ratios:
                     pr = self._probe_buffers(ratios[0])
@@ -466,7 +488,7 @@ class Session:
                     self._notify(ar_step, t, layer, q, outputs, blocks)
                 if final:
                     final_kv.append(blocks)
-                m = self.model.mix(layer, outputs)
+                m = self.model.mix(layer, self._gather_outputs(layer, outputs))
                 if m is not None:
                     x = m if x is None else x + m
             for r in ratios:
@@ -525,10 +547,10 @@ class Session:
             x = self.model.frame_input(ar_step, t)
             for layer in range(cfg.num_layers):
                 q, k, v = self._model_qkv(layer, x, ar_step, t)
-                blocks = [FrameBlock(ar_step, k[h], v[h]) for h in range(cfg.num_heads)]
+                blocks = [FrameBlock(ar_step, k[h], v[h]) for h in range(k.shape[0])]
                 outputs, lc = self._layer_attention(layer, q, self.caches[layer], blocks)
                 counters.add_layer(lc)
-                m = self.model.mix(layer, outputs)
+                m = self.model.mix(layer, self._gather_outputs(layer, outputs))
                 if m is not None:
                     x = m if x is None else x + m
             walls.append(counters.wall_time_ns)

@@ -211,3 +211,35 @@ def test_wan_layer_full_size_properties():
         k, v, _ = pruned[h].gather_context(cur[h])
         ref = torch.softmax((q[h].float() @ k.float().T) / math.sqrt(d), -1) @ v.float()
         assert (o_p[h].float() - ref).abs().max() / ref.abs().max() <= TOL
+
+
+def test_head_parallel_session_world1_matches_session():
+    """HeadParallelSession wiring on the NCCL backend (one rank on this GPU):
+    identical classes, scores and outputs to the plain Session."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2601_20499_b200.parallel import HeadParallelSession
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    try:
+        ocfg = O.Config(num_layers=2, num_heads=4, head_dim=64, HW=192, window_len=4, ar_steps=5, denoise_steps=1,
+                        dummy_count=3, probe_ar_step=2)
+        labels = ("sink", "neighbor", "current", "neighbor", "current", "sink", "neighbor", "current")
+        stream = O.PlantedStream(labels, 2.0, O.derive(2, "planted"), ocfg)
+        cfg = df.SessionConfig(**ocfg.__dict__)
+        a = df.Session(stream, cfg, "packed")
+        fa, ra = a.run()
+        b = HeadParallelSession(stream, cfg, "packed")
+        fb, rb = b.run()
+        assert a.assignment == b.assignment
+        assert ra.kernel_calls_steady == rb.kernel_calls_steady
+        assert ra.output_digest == rb.output_digest
+    finally:
+        dist.destroy_process_group()
