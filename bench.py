@@ -318,12 +318,37 @@ def gpu_arm(args, ws, rank, local):
     pinned = [tuple(x.cpu().pin_memory() for x in layer) for layer in inputs]
     outs_host = [torch.empty(H, HW, D, dtype=torch.bfloat16).pin_memory() for _ in range(L)]
 
+    # User-level pipelining around the public API: H2D of layer l+1 on a copy
+    # stream and D2H of layer l-1 on another overlap layer l's kernels.
+    ms = torch.cuda.current_stream(dev)
+    cs, ds = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    stage = [tuple(torch.empty(H, HW, D, dtype=torch.bfloat16, device=dev) for _ in range(3)) for _ in range(2)]
+    freed = [torch.cuda.Event() for _ in range(2)]
+    for e in freed:
+        e.record(ms)
+
     def e2e_step():
+        cs.wait_stream(ms)  # copies of this step start after the timing event
         for layer in range(L):
-            q, k, v = pinned[layer]
+            buf = stage[layer % 2]
+            ready = torch.cuda.Event()
+            with torch.cuda.stream(cs):
+                cs.wait_event(freed[layer % 2])
+                for dst, src in zip(buf, pinned[layer]):
+                    dst.copy_(src, non_blocking=True)
+                ready.record(cs)
+            ms.wait_event(ready)
+            q, k, v = buf
             blocks = [df.FrameBlock(W, k[h], v[h]) for h in range(H)]
             out, lc = df.packed_step(q, packed[layer], blocks, classes, cfg)
-            outs_host[layer].copy_(out, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(ms)
+            freed[layer % 2] = done
+            with torch.cuda.stream(ds):
+                ds.wait_event(done)
+                out.record_stream(ds)
+                outs_host[layer].copy_(out, non_blocking=True)
+        ms.wait_stream(ds)
         return []
 
     barrier(ws)
@@ -365,7 +390,9 @@ def gpu_arm(args, ws, rank, local):
                           "frac": pack_gbs / hbm_peak, "bytes": pack_bytes, "ms": min(pack_ms),
                           "kernel": "df_pack_kernel"},
         "e2e": {"value": fps_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": t_e2e, "path": "public packed_step with pinned host Q/K/V, D2H of outputs"},
+                "ms_per_step": t_e2e,
+                "path": "public packed_step per layer; pinned host Q/K/V H2D on a copy stream (double-buffered), "
+                        "outputs D2H on a second stream, all inside the timed region"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
