@@ -332,7 +332,9 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
       const float2 negm2 = make_float2(-m, -m);
       float2 sum2 = make_float2(0.f, 0.f);
       float span = 0.f;
+      float2 lo2 = make_float2(0.f, 0.f);  // probe fast path: mass left of the (single) slot boundary
       int next_b = 0, kind = 0, slot = 0;
+      const bool wide = p.hw >= kBN;       // a 128-key tile then spans at most two ring slots
       if constexpr (kProbe) {
         const int c0 = j * kBN;
         slot = min(c0 / p.hw, p.max_slots - 1);
@@ -356,18 +358,22 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
           sum2 = add2(sum2, e);
           pk[i] = pack_bf16x2(a, b);
           if constexpr (kProbe) {
+            if (wide) {
+              lo2 = add2(lo2, make_float2(c < next_b ? a : 0.f, c + 1 < next_b ? b : 0.f));
+            } else {
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              if (c + e == next_b) {  // warp-uniform region boundary
-                reg_acc[0] += kind == 0 ? span : 0.f;
-                reg_acc[1] += kind == 1 ? span : 0.f;
-                reg_acc[2] += kind == 2 ? span : 0.f;
-                span = 0.f;
-                next_b += p.hw;
-                slot = min(slot + 1, p.max_slots - 1);
-                kind = p.region_tab[h * p.max_slots + slot];
+              for (int e = 0; e < 2; ++e) {
+                if (c + e == next_b) {  // warp-uniform region boundary
+                  reg_acc[0] += kind == 0 ? span : 0.f;
+                  reg_acc[1] += kind == 1 ? span : 0.f;
+                  reg_acc[2] += kind == 2 ? span : 0.f;
+                  span = 0.f;
+                  next_b += p.hw;
+                  slot = min(slot + 1, p.max_slots - 1);
+                  kind = p.region_tab[h * p.max_slots + slot];
+                }
+                span += e ? b : a;
               }
-              span += e ? b : a;
             }
           }
         }
@@ -379,9 +385,17 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
         }
       }
       if constexpr (kProbe) {
-        reg_acc[0] += kind == 0 ? span : 0.f;
-        reg_acc[1] += kind == 1 ? span : 0.f;
-        reg_acc[2] += kind == 2 ? span : 0.f;
+        if (wide) {
+          const float lo = lo2.x + lo2.y, hi = (sum2.x + sum2.y) - lo;
+          const int kind1 = p.region_tab[h * p.max_slots + min(slot + 1, p.max_slots - 1)];
+          reg_acc[0] += (kind == 0 ? lo : 0.f) + (kind1 == 0 ? hi : 0.f);
+          reg_acc[1] += (kind == 1 ? lo : 0.f) + (kind1 == 1 ? hi : 0.f);
+          reg_acc[2] += (kind == 2 ? lo : 0.f) + (kind1 == 2 ? hi : 0.f);
+        } else {
+          reg_acc[0] += kind == 0 ? span : 0.f;
+          reg_acc[1] += kind == 1 ? span : 0.f;
+          reg_acc[2] += kind == 2 ? span : 0.f;
+        }
       }
       l += sum2.x + sum2.y;
       tmem_wait_st();

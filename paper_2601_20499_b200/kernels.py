@@ -16,7 +16,6 @@ from . import _lib
 from .errors import ShapeError
 
 TOKEN_ALIGN = 128  # head regions start on a kv-tile boundary
-SPLIT_KV = True  # provide a split-KV workspace (the C planner decides whether to split)
 SUPPORTED_WIDTHS = (64, 128)
 
 
@@ -190,7 +189,7 @@ def attention(
     handle = _stream_handle(stream)
     need = ctypes.c_int64(0)
     _lib.call("df_attn_workspace_bytes", ctypes.byref(args), ctypes.byref(need))
-    if need.value > 0 and SPLIT_KV:
+    if need.value > 0:
         ws = _split_workspace(q.device, handle.value, need.value)
         args.workspace = ws.data_ptr()
         args.workspace_bytes = ws.numel()
@@ -201,10 +200,10 @@ _WORKSPACES: dict[tuple[int, int], torch.Tensor] = {}
 
 
 def _split_workspace(device: torch.device, stream_handle: int, nbytes: int) -> torch.Tensor:
-    """Per-(device, stream) split-KV workspace, zero-filled at allocation.
+    """Per-(device, stream) stream-K workspace (split partials + combine counters).
 
-    The kernel returns every combine counter to zero, so the buffer can be
-    reused by the next launch on the same stream without a memset.
+    Zero-filled at allocation; the kernel returns every combine counter to
+    zero, so the next launch on the same stream reuses it without a memset.
     """
     key = (device.index if device.index is not None else torch.cuda.current_device(), stream_handle or 0)
     ws = _WORKSPACES.get(key)

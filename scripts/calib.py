@@ -5,7 +5,6 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2601_20499_b200 import kernels as K
 dev = torch.device('cuda:0'); D = 128
 def run(ctxs, HW, reps=10, split=True):
-    K.SPLIT_KV = split
     H = len(ctxs)
     arena = K.KVArena(sum(K.KVArena.region_rows(c) for c in ctxs), D, dev)
     arena.k.normal_(); arena.v.normal_()

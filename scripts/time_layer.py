@@ -26,6 +26,8 @@ def run(ctxs, HW=4680, reps=20, probe=False):
     t = e0.elapsed_time(e1) / reps
     return t * 1e3, 4 * D * HW * sum(ctxs) / (t * 1e-3) / 1e12
 cases = {
+ 'small_12x9360': ([9360] * 12, 4680),
+ 'small_2x32760': ([32760] * 2, 4680),
  'baseline_12x32760': ([32760] * 12, 4680),
  'packed_6d3s3n': ([28080] * 3 + [9360] * 9, 4680),
  'packed_3d4s5n': ([28080] * 5 + [9360] * 7, 4680),
