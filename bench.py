@@ -311,6 +311,15 @@ def gpu_arm(args, ws, rank, local):
                                  args.warmup)
     t_step = barrier_max(t_step, ws)
     attn_ns = [lc.attn_time_ns for step in lcs for lc in step]
+
+    # the same step replayed as one CUDA graph (no host work per layer)
+    sg = df.StepGraph(packed, cfg, frame_id=W, mode="packed", classes=[classes] * L)
+    for layer in range(L):
+        for dst, src in zip((sg.q[layer], sg.k[layer], sg.v[layer]), inputs[layer]):
+            dst.copy_(src)
+    t_graph, _ = time_steps(sg.replay, args.steps, args.warmup)
+    t_graph = barrier_max(t_graph, ws)
+    del sg
     layer_ns = [lc.wall_time_ns for step in lcs for lc in step]
     launches = sum(lc.physical_launches for step in lcs for lc in step)
 
@@ -376,6 +385,7 @@ def gpu_arm(args, ws, rank, local):
                    "assignment_per_layer": "6d/3s/3n", "l2": "inputs larger than L2 (no flush needed)",
                    "parallelism": f"independent streams x{ws} (no collective)"},
         "us_per_layer": t_step * 1e3 / L,
+        "graph_ms_per_step": t_graph,
         "attn_us_per_layer": attn_avg_s * 1e6,
         "tflops": achieved,
         "baseline_all_context": {"ms_per_step": t_base, "us_per_layer": t_base * 1e3 / L,

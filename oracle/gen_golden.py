@@ -242,6 +242,21 @@ def gen_toy_report():
     json.dump(out, open(os.path.join(OUT, "toy_c1_reports.json"), "w"))
 
 
+def gen_container():
+    """A small .dfc written by the reference's container.save_tensors."""
+    from dummy_forcing import container as ref_container
+
+    rng = np.random.default_rng(12)
+    tensors = {"layer0/head0/frame0/keys": rng.standard_normal((4, 8)).astype(np.float32),
+               "layer0/head0/frame0/values": rng.standard_normal((4, 8)),
+               "scalar": np.array(3.5)}
+    path = os.path.join(OUT, "ref_container.dfc")
+    ref_container.save_tensors(path, tensors)
+    json.dump({"digest": ref_container.array_digest(*tensors.values())},
+              open(os.path.join(OUT, "ref_container.json"), "w"))
+
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     gen_rng()
@@ -251,4 +266,6 @@ if __name__ == "__main__":
     gen_planted_sessions()
     gen_accounting()
     gen_toy_report()
+    gen_container()
     print("golden fixtures written to", OUT)
+

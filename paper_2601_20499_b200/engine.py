@@ -209,12 +209,13 @@ def _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, strea
 
 
 def baseline_step(q_heads, caches: list[HeadKVCache], current_blocks: list[FrameBlock], config: SessionConfig,
-                  *, stream=None, probe: ProbeRequest | None = None):
+                  *, stream=None, probe: ProbeRequest | None = None, timed: bool = True):
     """Full-window attention for every head of one layer (engine.py:140-152)."""
     for c in caches:
         if c.policy.kind != "baseline_window":
             raise ConfigError(f"baseline_step got a {c.policy.kind} cache")
-    return _dispatch(q_heads, caches, current_blocks, config.head_dim, [list(range(len(caches)))], probe, stream)
+    return _dispatch(q_heads, caches, current_blocks, config.head_dim, [list(range(len(caches)))], probe, stream,
+                     timed)
 
 
 def _class_groups(classes: list[HeadClass]) -> list[list[int]]:
@@ -222,15 +223,16 @@ def _class_groups(classes: list[HeadClass]) -> list[list[int]]:
 
 
 def hma_step(q_heads, caches, current_blocks, classes: list[HeadClass], config: SessionConfig, *, stream=None,
-             probe: ProbeRequest | None = None):
+             probe: ProbeRequest | None = None, timed: bool = True):
     """Class-specific contexts; logically one call per class present (engine.py:161-174)."""
     if len(classes) != len(caches):
         raise AssignmentError(f"{len(classes)} classes for {len(caches)} heads in this layer")
-    return _dispatch(q_heads, caches, current_blocks, config.head_dim, _class_groups(list(classes)), probe, stream)
+    return _dispatch(q_heads, caches, current_blocks, config.head_dim, _class_groups(list(classes)), probe, stream,
+                     timed)
 
 
 def packed_step(q_heads, caches, current_blocks, classes: list[HeadClass], config: SessionConfig, *, stream=None,
-                probe: ProbeRequest | None = None):
+                probe: ProbeRequest | None = None, timed: bool = True):
     """Dummy+sink share one logical call, neighbors the other (engine.py:177-195)."""
     if not config.packing_enabled:
         raise ConfigError("packed_step requires packing_enabled")
@@ -238,7 +240,7 @@ def packed_step(q_heads, caches, current_blocks, classes: list[HeadClass], confi
         raise AssignmentError(f"{len(classes)} classes for {len(caches)} heads in this layer")
     ds = [h for h, c in enumerate(classes) if c is not HeadClass.NEIGHBOR]
     nb = [h for h, c in enumerate(classes) if c is HeadClass.NEIGHBOR]
-    return _dispatch(q_heads, caches, current_blocks, config.head_dim, [ds, nb], probe, stream)
+    return _dispatch(q_heads, caches, current_blocks, config.head_dim, [ds, nb], probe, stream, timed)
 
 
 def expected_step_macs(config: SessionConfig, mode: str, history_frames: int,
@@ -595,6 +597,65 @@ class Session:
             output_digest=_digest(self._frames),
             physical_launches_steady=self._phys_last,
         )
+
+
+class StepGraph:
+    """One denoise iteration over every layer, captured once as a CUDA graph.
+
+    SURVEY.md 8(f) row 3 (Session._run_step / time_step, engine.py:407-550):
+    the per-layer Python dispatch (staging copy + ragged FMHA launch) is
+    recorded for a fixed cache state and replayed with no host work.  Inputs
+    are the static device buffers ``q[l]``, ``k[l]``, ``v[l]`` (heads, HW, d)
+    -- copy the iteration's projections into them (or have the producer
+    write there) and call :meth:`replay`; ``outputs[l]`` hold the results.
+    A graph stays valid while the caches' slot tables do not change, i.e.
+    for every denoise iteration of one AR step (the cache is appended only
+    after the final iteration, engine.py:457-463).
+    """
+
+    def __init__(self, caches: list[list[HeadKVCache]], config: SessionConfig, frame_id: int, mode: str = "baseline",
+                 classes: list[list[HeadClass]] | None = None, device=None):
+        if mode not in MODES:
+            raise ConfigError(f"unknown mode {mode!r}")
+        self.config = config
+        self.caches = caches
+        self.mode = mode
+        self.classes = classes
+        self.frame_id = frame_id
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        cfg = config
+        H = len(caches[0])
+        shape = (H, cfg.HW, cfg.head_dim)
+        self.q = [torch.zeros(shape, dtype=torch.bfloat16, device=dev) for _ in caches]
+        self.k = [torch.zeros(shape, dtype=torch.bfloat16, device=dev) for _ in caches]
+        self.v = [torch.zeros(shape, dtype=torch.bfloat16, device=dev) for _ in caches]
+        self.outputs: list[torch.Tensor] = []
+        self.graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            self._launch_all()  # eager warm-up: allocates the stream's workspace, checks every error path
+        torch.cuda.current_stream(dev).wait_stream(side)
+        with torch.cuda.graph(self.graph, stream=side):
+            self.outputs = self._launch_all()
+        self.kernel_launches = 2 * len(caches)
+
+    def _launch_all(self) -> list[torch.Tensor]:
+        outs = []
+        for layer, caches in enumerate(self.caches):
+            blocks = [FrameBlock(self.frame_id, self.k[layer][h], self.v[layer][h]) for h in range(len(caches))]
+            if self.mode == "baseline" or self.classes is None:
+                o, _ = baseline_step(self.q[layer], caches, blocks, self.config, timed=False)
+            elif self.mode == "hma":
+                o, _ = hma_step(self.q[layer], caches, blocks, self.classes[layer], self.config, timed=False)
+            else:
+                o, _ = packed_step(self.q[layer], caches, blocks, self.classes[layer], self.config, timed=False)
+            outs.append(o)
+        return outs
+
+    def replay(self) -> list[torch.Tensor]:
+        self.graph.replay()
+        return self.outputs
 
 
 def generate_session(model, config: SessionConfig, mode: str = "baseline",

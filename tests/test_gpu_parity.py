@@ -243,3 +243,50 @@ def test_head_parallel_session_world1_matches_session():
         assert ra.output_digest == rb.output_digest
     finally:
         dist.destroy_process_group()
+
+
+def test_step_graph_replay_matches_eager():
+    """CUDA-graph capture of a denoise iteration: replays are
+    bitwise equal to the eager public-API step, with fresh inputs each replay."""
+    L, H, HW, d, W = 2, 4, 300, 128, 4
+    cfg = df.SessionConfig(num_layers=L, num_heads=H, head_dim=d, HW=HW, window_len=W, ar_steps=W + 2, dummy_count=2)
+    g = torch.Generator(device=DEV).manual_seed(3)
+    rnd = lambda *s: torch.randn(*s, device=DEV, generator=g).to(torch.bfloat16)
+    caches = []
+    for layer in range(L):
+        row = []
+        for h in range(H):
+            c = df.HeadKVCache(df.baseline_policy(cfg))
+            for f in range(W):
+                c.append_and_evict(df.FrameBlock(f, rnd(HW, d), rnd(HW, d)))
+            row.append(c)
+        caches.append(row)
+    classes = [df.HeadClass.DUMMY, df.HeadClass.SINK, df.HeadClass.NEIGHBOR, df.HeadClass.NEIGHBOR]
+    packed = [df.rebuild_caches(row, [df.derive_policy(c, cfg) for c in classes]) for row in caches]
+    sg = df.StepGraph(packed, cfg, frame_id=W, mode="packed", classes=[classes] * L)
+    for _ in range(2):
+        for layer in range(L):
+            for buf in (sg.q[layer], sg.k[layer], sg.v[layer]):
+                buf.copy_(rnd(H, HW, d))
+        outs = [o.clone() for o in sg.replay()]
+        for layer in range(L):
+            blocks = [df.FrameBlock(W, sg.k[layer][h], sg.v[layer][h]) for h in range(H)]
+            ref, _ = df.packed_step(sg.q[layer], packed[layer], blocks, classes, cfg)
+            assert torch.equal(outs[layer], ref)
+
+
+def test_session_cache_snapshot_container(tmp_path):
+    from paper_2601_20499_b200 import container as C
+
+    ocfg = O.Config(num_layers=1, num_heads=4, head_dim=64, HW=64, window_len=3, ar_steps=5, denoise_steps=1,
+                    dummy_count=1, probe_ar_step=2)
+    stream = O.PlantedStream(("sink", "neighbor", "current", "neighbor"), 2.0, O.derive(4, "planted"), ocfg)
+    s = df.Session(stream, df.SessionConfig(**ocfg.__dict__), "packed")
+    s.run()
+    path = str(tmp_path / "cache.dfc")
+    C.save_cache_snapshot(path, s.caches)
+    back = C.load_tensors(path)
+    snap = df.cache_snapshot(s.caches)
+    assert set(back) == set(snap) and len(snap) > 0
+    for name, t in snap.items():
+        np.testing.assert_array_equal(back[name], t.float().cpu().numpy())

@@ -174,3 +174,25 @@ def test_layout_and_scores_helpers():
     assert (s.alpha_sink, s.alpha_neighbor, s.alpha_current) == (0.25, 0.5, 0.25)
     with pytest.raises(df.ShapeError):
         df.frame_attention_scores(np.full((2, 8), 1 / 8), lay)
+
+
+def test_container_byte_compatible_with_reference(tmp_path):
+    from paper_2601_20499_b200 import container as C
+
+    g = os.path.join(G, "ref_container.dfc")
+    t = C.load_tensors(g)  # written by the reference's save_tensors
+    assert set(t) == {"layer0/head0/frame0/keys", "layer0/head0/frame0/values", "scalar"}
+    assert t["layer0/head0/frame0/keys"].dtype == np.float32 and t["scalar"].shape == (1,)  # as the reference writes 0-d
+    want = json.load(open(os.path.join(G, "ref_container.json")))["digest"]
+    assert C.array_digest(*t.values()) == want
+    out = tmp_path / "re.dfc"
+    C.save_tensors(str(out), t)
+    assert open(out, "rb").read() == open(g, "rb").read()  # byte-identical rewrite
+    # bf16 tensors widen exactly to f32
+    x = torch.randn(3, 5).to(torch.bfloat16)
+    C.save_tensors(str(out), {"x": x})
+    np.testing.assert_array_equal(C.load_tensors(str(out))["x"], x.float().numpy())
+    with pytest.raises(df.ConfigError):
+        bad = tmp_path / "bad.dfc"
+        bad.write_bytes(b"\x01")
+        C.load_tensors(str(bad))
