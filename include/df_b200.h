@@ -61,10 +61,13 @@ extern "C" {
 #define DF_MAX_HEADS 64     /* heads per df_attn_fwd launch */
 #define DF_MAX_ARENAS 4     /* distinct KV arenas per launch */
 #define DF_TMAP_BYTES 128   /* one CUtensorMap */
+#define DF_MAPS_PER_ARENA 3 /* K (128-row box), V (128-row box), K (64-row box) */
 #define DF_MAX_APPEND_SEGS 128
 
 /* df_attn_args.flags */
-#define DF_ATTN_PROBE 1u    /* fused DHP region-mass epilogue */
+#define DF_ATTN_PROBE 1u       /* fused DHP region-mass epilogue */
+#define DF_ATTN_PAIR 2u        /* d = 128: CTA-pair (cta_group::2, M = 256) kernel */
+#define DF_ATTN_SINGLE_CTA 4u  /* force the 1-CTA kernel */
 
 /* One head of one layer.  Its context is the contiguous token range
  * [base_row, base_row + n_tok) of arena `arena` (K and V share row indices);
@@ -90,7 +93,7 @@ typedef struct df_attn_args {
   int32_t num_heads;      /* <= DF_MAX_HEADS */
   int32_t num_arenas;     /* <= DF_MAX_ARENAS */
   const df_head_desc* heads;  /* host [num_heads] */
-  const uint8_t* kv_maps;     /* host [num_arenas][2][DF_TMAP_BYTES] from df_kv_arena_maps */
+  const uint8_t* kv_maps;     /* host [num_arenas][DF_MAPS_PER_ARENA][DF_TMAP_BYTES] from df_kv_arena_maps */
   uint32_t flags;
   int32_t max_slots;              /* probe: row stride of region_of_slot */
   const uint8_t* region_of_slot;  /* probe, device [num_heads][max_slots]; 0 sink 1 neighbor 2 current */
@@ -119,8 +122,8 @@ DF_API int df_attn_fwd(const df_attn_args* args, void* stream);
  * device's SMs); 0 when no head is split. */
 DF_API int df_attn_workspace_bytes(const df_attn_args* args, int64_t* bytes);
 
-/* TMA descriptors (K map then V map, 2*DF_TMAP_BYTES bytes) of an arena whose
- * K and V planes are device bf16 [rows][head_dim]. */
+/* TMA descriptors (DF_MAPS_PER_ARENA*DF_TMAP_BYTES bytes: K, V, K-half maps)
+ * of an arena whose K and V planes are device bf16 [rows][head_dim]. */
 DF_API int df_kv_arena_maps(const void* k_base, const void* v_base, int64_t rows,
                      int32_t head_dim, uint8_t* out_maps);
 

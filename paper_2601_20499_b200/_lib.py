@@ -28,8 +28,11 @@ DF_E_ARG = 7
 DF_MAX_HEADS = 64
 DF_MAX_ARENAS = 4
 DF_TMAP_BYTES = 128
+DF_MAPS_PER_ARENA = 3
 DF_MAX_APPEND_SEGS = 128
 DF_ATTN_PROBE = 1
+DF_ATTN_PAIR = 2
+DF_ATTN_SINGLE_CTA = 4
 
 _CODE_TO_EXC = {
     DF_E_SHAPE: errors.ShapeError,

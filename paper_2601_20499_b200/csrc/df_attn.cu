@@ -64,7 +64,7 @@ struct HeadParam {
 
 struct __align__(64) AttnParams {
   CUtensorMap qmap;
-  CUtensorMap kvmap[2 * DF_MAX_ARENAS];
+  CUtensorMap kvmap[DF_MAPS_PER_ARENA * DF_MAX_ARENAS];
   __nv_bfloat16* out;
   const uint8_t* region_tab;
   const uint8_t* row_sampled;
@@ -99,6 +99,11 @@ struct AttnCfg {
   static constexpr int kSmem = kBarOff + kNumBars * 8 + 32 + 1024;  // + 1 KB alignment slack
   static constexpr uint32_t kTmemO = 256;
 };
+
+// named barrier of one softmax warpgroup (ids 2, 3; id 1 spans both groups)
+__device__ __forceinline__ void wg_bar_sync(int id) {
+  asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
+}
 
 __device__ __forceinline__ void softmax_bar_sync(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
@@ -165,8 +170,8 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      const void* kmap = &p.kvmap[2 * hd.arena];
-      const void* vmap = &p.kvmap[2 * hd.arena + 1];
+      const void* kmap = &p.kvmap[DF_MAPS_PER_ARENA * hd.arena];
+      const void* vmap = &p.kvmap[DF_MAPS_PER_ARENA * hd.arena + 1];
       prefetch_tmap(&p.qmap);
       prefetch_tmap(kmap);
       prefetch_tmap(vmap);
@@ -513,6 +518,469 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
   }
 }
 
+// =====================================================================
+// CTA-pair variant (cta_group::2, d = 128).  A cluster of two CTAs on one
+// TPC computes M = 256 per MMA: each CTA owns 128 rows of every 256-row query
+// tile, half of every K tile (64 keys) and half of every V tile (64 columns);
+// the leader's single thread issues tcgen05.mma.cta_group::2 for both.  Per SM
+// this halves the K/V bytes staged by TMA and read by the tensor core, which
+// otherwise keep the shared-memory port saturated during QK^T.  Work item =
+// (head, 512 query rows, kv piece); MMA tile t covers rows [t*256, t*256+256)
+// of the item, CTA rank r rows [t*256 + r*128, +128).
+struct PairCfg {
+  static constexpr int D = 128;
+  static constexpr int kStages = 4;                      // K and V ring depth
+  static constexpr int kQTileBytes = 128 * D * 2;        // this CTA's rows of one MMA tile
+  static constexpr int kQBoxBytes = 128 * 128;           // [128 rows x 64 cols]
+  static constexpr int kKHalfBytes = 64 * D * 2;         // 64 keys x d
+  static constexpr int kKBoxBytes = 64 * 128;            // [64 rows x 64 cols]
+  static constexpr int kVHalfBytes = 128 * 64 * 2;       // 128 keys x 64 columns
+  static constexpr int kQOff = 0;
+  static constexpr int kKOff = 2 * kQTileBytes;
+  static constexpr int kVOff = kKOff + kStages * kKHalfBytes;
+  static constexpr int kBarOff = kVOff + kStages * kVHalfBytes;
+  static constexpr int kNumBars = 1 + 4 * kStages + 2 + 4 + 2;
+  static constexpr int kSmem = kBarOff + kNumBars * 8 + 32 + 1024;
+  static constexpr uint32_t kTmemO = 256;
+};
+
+template <bool kProbe>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    df_attn_pair_kernel(const __grid_constant__ AttnParams p) {
+  using C = PairCfg;
+  constexpr int D = C::D;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = q_full + 1;
+  uint64_t* k_empty = k_full + C::kStages;
+  uint64_t* v_full = k_empty + C::kStages;
+  uint64_t* v_empty = v_full + C::kStages;
+  uint64_t* s_full = v_empty + C::kStages;  // [2]
+  uint64_t* p_full = s_full + 2;            // [2 tiles][2 halves], leader: 128 + 128 arrivals
+  uint64_t* o_full = p_full + 4;            // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+  int32_t* last_flag = reinterpret_cast<int32_t*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1;
+  int hrank = 0;
+  while (hrank + 1 < p.n_heads && p.item_prefix[hrank + 1] <= pair) ++hrank;
+  const int h = p.head_order[hrank];
+  const HeadParam hd = p.heads[h];
+  const int local = pair - p.item_prefix[hrank];
+  const int ns = hd.n_split;
+  const int qp = local / ns;
+  const int piece = local - qp * ns;
+  const int n_kv_total = (hd.n_tok + kBN - 1) / kBN;
+  const int kv_begin = (piece * n_kv_total) / ns;
+  const int n_kv = ((piece + 1) * n_kv_total) / ns - kv_begin;
+  const bool two = qp * 4 * kBM + 2 * kBM < p.hw;  // second 256-row tile has rows
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(k_full + s, 1);
+      mbar_init(k_empty + s, 1);
+      mbar_init(v_full + s, 1);
+      mbar_init(v_empty + s, 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(s_full + t, 1);
+      mbar_init(p_full + 2 * t, 2);  // one arrival per CTA of the pair
+      mbar_init(p_full + 2 * t + 1, 2);
+      mbar_init(o_full + t, 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      const void* kmap = &p.kvmap[DF_MAPS_PER_ARENA * hd.arena + 2];  // 64-row boxes
+      const void* vmap = &p.kvmap[DF_MAPS_PER_ARENA * hd.arena + 1];
+      prefetch_tmap(&p.qmap);
+      prefetch_tmap(kmap);
+      prefetch_tmap(vmap);
+      const uint64_t keep = policy_evict_last();
+      const int nq = two ? 2 : 1;
+      const int qrow0 = hd.q_head * p.hw + qp * 4 * kBM + static_cast<int>(crank) * kBM;
+      if (crank == 0) mbar_expect_tx(q_full, nq * 2 * C::kQTileBytes);
+      const uint32_t lq = mapa_shared(smem_u32(q_full), 0);
+      for (int t = 0; t < nq; ++t)
+        for (int b = 0; b < 2; ++b)
+          tma_load_2d_pair(smem + C::kQOff + t * C::kQTileBytes + b * C::kQBoxBytes, &p.qmap, lq, b * 64,
+                           qrow0 + t * 2 * kBM, keep);
+      for (int jj = 0; jj < n_kv; ++jj) {
+        const int row = hd.base_row + (kv_begin + jj) * kBN;
+        const int s = jj % C::kStages;
+        const uint32_t ph = (jj / C::kStages) & 1;
+        mbar_wait_cluster(k_empty + s, ph ^ 1);
+        if (crank == 0) mbar_expect_tx(k_full + s, 2 * C::kKHalfBytes);
+        const uint32_t lk = mapa_shared(smem_u32(k_full + s), 0);
+        for (int b = 0; b < 2; ++b)
+          tma_load_2d_pair(smem + C::kKOff + s * C::kKHalfBytes + b * C::kKBoxBytes, kmap, lk, b * 64,
+                           row + static_cast<int>(crank) * 64, keep);
+        mbar_wait_cluster(v_empty + s, ph ^ 1);
+        if (crank == 0) mbar_expect_tx(v_full + s, 2 * C::kVHalfBytes);
+        const uint32_t lv = mapa_shared(smem_u32(v_full + s), 0);
+        tma_load_2d_pair(smem + C::kVOff + s * C::kVHalfBytes, vmap, lv, static_cast<int>(crank) * 64, row, keep);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA)
+    if (lane == 0 && crank == 0) {
+      constexpr uint32_t idesc_qk = idesc_bf16(2 * kBM, kBN, false);
+      constexpr uint32_t idesc_pv = idesc_bf16(2 * kBM, D, true);
+      const uint32_t sQ = smem_u32(smem + C::kQOff);
+      const uint32_t sK = smem_u32(smem + C::kKOff);
+      const uint32_t sV = smem_u32(smem + C::kVOff);
+      const uint32_t tS0 = tmem, tS1 = tmem + 128;
+      const uint32_t tO0 = tmem + C::kTmemO, tO1 = tmem + C::kTmemO + D;
+
+      auto qk = [&](uint32_t d_tmem, int t, int ks) {
+        const uint32_t qa = sQ + t * C::kQTileBytes;
+        const uint32_t kb = sK + ks * C::kKHalfBytes;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t oa = (kk >> 2) * C::kQBoxBytes + (kk & 3) * 32;
+          const uint32_t ob = (kk >> 2) * C::kKBoxBytes + (kk & 3) * 32;
+          umma_ss_pair(d_tmem, sdesc_sw128(qa + oa, 16, 1024), sdesc_sw128(kb + ob, 16, 1024), idesc_qk, kk > 0);
+        }
+      };
+      auto pv = [&](int t, int jj) {
+        const int vs = jj % C::kStages;
+        mbar_wait_cluster(p_full + 2 * t, jj & 1);
+        tc_fence_after();
+        if (t == 0) {
+          mbar_wait_cluster(v_full + vs, (jj / C::kStages) & 1);
+          tc_fence_after();
+        }
+        const uint32_t vb = sV + vs * C::kVHalfBytes;
+        const uint32_t tP = t ? tS1 : tS0;
+        const uint32_t tO = t ? tO1 : tO0;
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          if (kk == kBN / 32) {
+            mbar_wait_cluster(p_full + 2 * t + 1, jj & 1);
+            tc_fence_after();
+          }
+          umma_ts_pair(tO, tP + kk * 8, sdesc_sw128(vb + kk * 2048, 16, 1024), idesc_pv,
+                       (jj > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit_pair(o_full + t);
+        if (t == 1 || !two) umma_commit_pair(v_empty + vs);
+      };
+
+      mbar_wait_cluster(q_full, 0);
+      tc_fence_after();
+      for (int jj = 0; jj < n_kv; ++jj) {
+        const int ks = jj % C::kStages;
+        mbar_wait_cluster(k_full + ks, (jj / C::kStages) & 1);
+        tc_fence_after();
+        qk(tS0, 0, ks);
+        umma_commit_pair(s_full + 0);
+        if (two) {
+          if (jj > 0) pv(1, jj - 1);
+          qk(tS1, 1, ks);
+          umma_commit_pair(s_full + 1);
+        }
+        umma_commit_pair(k_empty + ks);
+        pv(0, jj);
+      }
+      if (two) pv(1, n_kv - 1);
+    }
+  } else if (warp >= 4 && (two || warp < 8)) {
+    // ------------------------------------------------------------ softmax (both CTAs)
+    const int t = (warp - 4) >> 2;
+    const int quad = warp & 3;
+    const int row_local = quad * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t tS = tmem + lane_off + t * 128;
+    const uint32_t tO = tmem + lane_off + C::kTmemO + t * D;
+    const uint32_t lp0 = mapa_shared(smem_u32(p_full + 2 * t), 0);
+    const uint32_t lp1 = mapa_shared(smem_u32(p_full + 2 * t + 1), 0);
+    const float sl2 = p.scale_log2;
+    float m = -INFINITY;
+    float l = 0.f;
+    float reg_acc[3] = {0.f, 0.f, 0.f};
+
+    for (int jj = 0; jj < n_kv; ++jj) {
+      const int j = kv_begin + jj;
+      mbar_wait_cluster(s_full + t, jj & 1);
+      tc_fence_after();
+      uint32_t r[128];
+      tmem_ld32(tS + 0, r + 0);
+      tmem_ld32(tS + 32, r + 32);
+      tmem_ld32(tS + 64, r + 64);
+      tmem_ld32(tS + 96, r + 96);
+      tmem_wait_ld();
+      const int valid = hd.n_tok - j * kBN;
+      if (valid < kBN) {
+#pragma unroll
+        for (int c = 0; c < 128; ++c)
+          if (c >= valid) r[c] = __float_as_uint(-INFINITY);
+      }
+      float mx0 = __uint_as_float(r[0]), mx1 = __uint_as_float(r[1]);
+      float mx2 = __uint_as_float(r[2]), mx3 = __uint_as_float(r[3]);
+#pragma unroll
+      for (int c = 4; c < 128; c += 4) {
+        mx0 = fmaxf(mx0, __uint_as_float(r[c + 0]));
+        mx1 = fmaxf(mx1, __uint_as_float(r[c + 1]));
+        mx2 = fmaxf(mx2, __uint_as_float(r[c + 2]));
+        mx3 = fmaxf(mx3, __uint_as_float(r[c + 3]));
+      }
+      const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+      if (jj == 0) {
+        m = m_tile;
+      } else {
+        const bool need = m_tile > m + kRescaleThreshold;
+        if (__any_sync(0xffffffffu, need)) {
+          const float alpha = need ? ex2(m - m_tile) : 1.f;
+          if (need) m = m_tile;
+          l *= alpha;
+          if constexpr (kProbe) {
+            reg_acc[0] *= alpha;
+            reg_acc[1] *= alpha;
+            reg_acc[2] *= alpha;
+          }
+          mbar_wait_cluster(o_full + t, (jj - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < D / 16; ++c) {
+            uint32_t o[16];
+            tmem_ld16(tO + c * 16, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st16(tO + c * 16, o);
+          }
+          tmem_wait_st();
+        }
+      }
+      const float2 scale2 = make_float2(sl2, sl2);
+      const float2 negm2 = make_float2(-m, -m);
+      float2 sum2 = make_float2(0.f, 0.f);
+      float2 lo2 = make_float2(0.f, 0.f);
+      float span = 0.f;
+      int next_b = 0, kind = 0, slot = 0;
+      const bool wide = p.hw >= kBN;
+      if constexpr (kProbe) {
+        const int c0 = j * kBN;
+        slot = min(c0 / p.hw, p.max_slots - 1);
+        next_b = (c0 / p.hw + 1) * p.hw - c0;
+        kind = p.region_tab[h * p.max_slots + slot];
+      }
+#pragma unroll
+      for (int quarter = 0; quarter < 4; ++quarter) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int c = quarter * 32 + 2 * i;
+          const float2 x = fma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
+          float2 e;
+          if ((c / 2) % kEmuEvery == kEmuEvery - 1) {
+            e = exp2_poly2(x);
+          } else {
+            e = make_float2(ex2(x.x), ex2(x.y));
+          }
+          sum2 = add2(sum2, e);
+          pk[i] = pack_bf16x2(e.x, e.y);
+          if constexpr (kProbe) {
+            if (wide) {
+              lo2 = add2(lo2, make_float2(c < next_b ? e.x : 0.f, c + 1 < next_b ? e.y : 0.f));
+            } else {
+#pragma unroll
+              for (int k2 = 0; k2 < 2; ++k2) {
+                if (c + k2 == next_b) {
+                  reg_acc[0] += kind == 0 ? span : 0.f;
+                  reg_acc[1] += kind == 1 ? span : 0.f;
+                  reg_acc[2] += kind == 2 ? span : 0.f;
+                  span = 0.f;
+                  next_b += p.hw;
+                  slot = min(slot + 1, p.max_slots - 1);
+                  kind = p.region_tab[h * p.max_slots + slot];
+                }
+                span += k2 ? e.y : e.x;
+              }
+            }
+          }
+        }
+        tmem_st16(tS + quarter * 16, pk);
+        if (quarter == 1) {
+          tmem_wait_st();
+          tc_fence_before();
+          wg_bar_sync(2 + t);  // all 128 rows of this CTA's P half written
+          if (row_local == 0) mbar_arrive_cluster(lp0);
+        }
+      }
+      if constexpr (kProbe) {
+        if (wide) {
+          const float lo = lo2.x + lo2.y, hi = (sum2.x + sum2.y) - lo;
+          const int kind1 = p.region_tab[h * p.max_slots + min(slot + 1, p.max_slots - 1)];
+          reg_acc[0] += (kind == 0 ? lo : 0.f) + (kind1 == 0 ? hi : 0.f);
+          reg_acc[1] += (kind == 1 ? lo : 0.f) + (kind1 == 1 ? hi : 0.f);
+          reg_acc[2] += (kind == 2 ? lo : 0.f) + (kind1 == 2 ? hi : 0.f);
+        } else {
+          reg_acc[0] += kind == 0 ? span : 0.f;
+          reg_acc[1] += kind == 1 ? span : 0.f;
+          reg_acc[2] += kind == 2 ? span : 0.f;
+        }
+      }
+      l += sum2.x + sum2.y;
+      tmem_wait_st();
+      tc_fence_before();
+      wg_bar_sync(2 + t);
+      if (row_local == 0) mbar_arrive_cluster(lp1);
+    }
+
+    // ------------------------------------------------------------ epilogue
+    mbar_wait_cluster(o_full + t, (n_kv - 1) & 1);
+    tc_fence_after();
+    const int prow = t * kBM + row_local;                                       // row within this CTA's 256
+    const int row = qp * 4 * kBM + t * 2 * kBM + static_cast<int>(crank) * kBM + row_local;  // row within the head
+    const bool row_ok = row < p.hw;
+    __nv_bfloat16* orow = p.out + (static_cast<int64_t>(hd.o_head) * p.hw + row) * p.out_ld;
+    auto store_row = [&](const float* o, int c0, float scale) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int col = c0 + v * 8;
+        if (col < p.d_out) {
+          uint4 wv;
+          wv.x = pack_bf16x2(o[v * 8 + 0] * scale, o[v * 8 + 1] * scale);
+          wv.y = pack_bf16x2(o[v * 8 + 2] * scale, o[v * 8 + 3] * scale);
+          wv.z = pack_bf16x2(o[v * 8 + 4] * scale, o[v * 8 + 5] * scale);
+          wv.w = pack_bf16x2(o[v * 8 + 6] * scale, o[v * 8 + 7] * scale);
+          *reinterpret_cast<uint4*>(orow + col) = wv;
+        }
+      }
+    };
+    if (ns == 1) {
+      const float inv_l = 1.f / l;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t o[32];
+        tmem_ld32(tO + c * 32, o);
+        tmem_wait_ld();
+        if (row_ok) store_row(reinterpret_cast<const float*>(o), c * 32, inv_l);
+      }
+      if constexpr (kProbe) {
+        if (row_ok && p.row_sampled[row]) {
+          float* dst = p.probe_rows + (static_cast<int64_t>(h) * p.hw + row) * 3;
+          dst[0] = reg_acc[0] * inv_l;
+          dst[1] = reg_acc[1] * inv_l;
+          dst[2] = reg_acc[2] * inv_l;
+        }
+      }
+    } else {
+      // split-KV, per CTA of the pair: slot (piece, rank), counter (group, rank)
+      const int group = (hd.group_base + qp) * 2 + static_cast<int>(crank);
+      const int64_t slot0 = static_cast<int64_t>(hd.part_base) + static_cast<int64_t>(qp) * ns;
+      auto slot_of = [&](int i) { return (slot0 + i) * 2 + crank; };
+      float* my_o = p.ws_o + (slot_of(piece) * 2 * kBM + prow) * D;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t o[32];
+        tmem_ld32(tO + c * 32, o);
+        tmem_wait_ld();
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          __stcg(reinterpret_cast<float4*>(my_o + c * 32 + v * 4),
+                 make_float4(__uint_as_float(o[4 * v]), __uint_as_float(o[4 * v + 1]), __uint_as_float(o[4 * v + 2]),
+                             __uint_as_float(o[4 * v + 3])));
+      }
+      float* my_ml = p.ws_ml + (slot_of(piece) * 2 * kBM + prow) * 8;
+      __stcg(reinterpret_cast<float4*>(my_ml), make_float4(m, l, reg_acc[0], reg_acc[1]));
+      __stcg(my_ml + 4, reg_acc[2]);
+      __threadfence();
+      const int nthreads = two ? 256 : 128;
+      softmax_bar_sync(nthreads);
+      if (threadIdx.x == 128) {
+        const int prev = atomicAdd(p.ws_cnt + group, 1);
+        *last_flag = (prev == ns - 1);
+        if (prev == ns - 1) p.ws_cnt[group] = 0;
+        __threadfence();
+      }
+      softmax_bar_sync(nthreads);
+      if (*last_flag && row_ok) {
+        float M = -INFINITY;
+        for (int i = 0; i < ns; ++i) M = fmaxf(M, __ldcg(p.ws_ml + (slot_of(i) * 2 * kBM + prow) * 8));
+        float den = 0.f;
+        float racc[3] = {0.f, 0.f, 0.f};
+        for (int i = 0; i < ns; ++i) {
+          const float* ml = p.ws_ml + (slot_of(i) * 2 * kBM + prow) * 8;
+          const float ei = ex2(__ldcg(ml) - M);
+          den += ei * __ldcg(ml + 1);
+          if constexpr (kProbe) {
+            racc[0] += ei * __ldcg(ml + 2);
+            racc[1] += ei * __ldcg(ml + 3);
+            racc[2] += ei * __ldcg(ml + 4);
+          }
+        }
+        const float inv = 1.f / den;
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+          float acc[32];
+#pragma unroll
+          for (int q = 0; q < 32; ++q) acc[q] = 0.f;
+          for (int i = 0; i < ns; ++i) {
+            const float ei = ex2(__ldcg(p.ws_ml + (slot_of(i) * 2 * kBM + prow) * 8) - M);
+            const float* src = p.ws_o + (slot_of(i) * 2 * kBM + prow) * D + c * 32;
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              const float4 x = __ldcg(reinterpret_cast<const float4*>(src + v * 4));
+              acc[4 * v + 0] += ei * x.x;
+              acc[4 * v + 1] += ei * x.y;
+              acc[4 * v + 2] += ei * x.z;
+              acc[4 * v + 3] += ei * x.w;
+            }
+          }
+          store_row(acc, c * 32, inv);
+        }
+        if constexpr (kProbe) {
+          if (p.row_sampled[row]) {
+            float* dst = p.probe_rows + (static_cast<int64_t>(h) * p.hw + row) * 3;
+            dst[0] = racc[0] * inv;
+            dst[1] = racc[1] * inv;
+            dst[2] = racc[2] * inv;
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer's smem and TMEM stay live until the leader's MMAs are done
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, 512);
+  }
+}
+
+template <bool kProbe>
+static int launch_attn_pair(const AttnParams& p, int grid, cudaStream_t stream) {
+  auto kern = df_attn_pair_kernel<kProbe>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg::kSmem);
+    if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(df_attn_pair_kernel)", e);
+    configured = true;
+  }
+  kern<<<grid, kThreads, PairCfg::kSmem, stream>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error("df_attn_pair_kernel launch", e);
+  return DF_OK;
+}
+
 template <int D, bool kProbe>
 static int launch_attn(const AttnParams& p, int grid, cudaStream_t stream) {
   using C = AttnCfg<D>;
@@ -565,9 +1033,13 @@ int sm_count_cached() {
   return count;
 }
 
-double simulate(const df_attn_args* a, const uint8_t* ns, const int* order, int sms) {
-  const int nq = (a->hw + 255) / 256;
-  const bool last_single = (nq - 1) * 256 + 128 >= a->hw;
+// rows of one work item: a pair of 128-row tiles, or 2 x 256 rows for the CTA-pair kernel
+inline int item_rows(bool pair) { return pair ? 512 : 256; }
+
+double simulate(const df_attn_args* a, const uint8_t* ns, const int* order, int sms, bool pair) {
+  const int R = item_rows(pair);
+  const int nq = (a->hw + R - 1) / R;
+  const bool last_single = (nq - 1) * R + R / 2 >= a->hw;
   std::priority_queue<double, std::vector<double>, std::greater<double>> bins;
   for (int i = 0; i < sms; ++i) bins.push(0.0);
   double makespan = 0.0;
@@ -598,8 +1070,9 @@ void order_heads(const df_attn_args* a, const uint8_t* ns, int* order) {
   });
 }
 
-int64_t workspace_need(const df_attn_args* a, const uint8_t* ns) {
-  const int nq = (a->hw + 255) / 256;
+int64_t workspace_need(const df_attn_args* a, const uint8_t* ns, bool pair) {
+  const int R = item_rows(pair);
+  const int nq = (a->hw + R - 1) / R;
   int64_t groups = 0, slots = 0;
   for (int h = 0; h < a->num_heads; ++h)
     if (ns[h] > 1) {
@@ -607,16 +1080,17 @@ int64_t workspace_need(const df_attn_args* a, const uint8_t* ns) {
       slots += int64_t(nq) * ns[h];
     }
   if (!groups) return 0;
-  const int64_t cnt_bytes = ((groups * 4 + 255) / 256) * 256;
-  return cnt_bytes + slots * 256 * (int64_t(a->head_dim) + 2) * 4;
+  const int64_t ranks = pair ? 2 : 1;
+  const int64_t cnt_bytes = ((groups * ranks * 4 + 255) / 256) * 256;
+  return cnt_bytes + slots * ranks * 256 * (int64_t(a->head_dim) + 8) * 4;
 }
 
-Plan make_plan(const df_attn_args* a, bool allow_split) {
+Plan make_plan(const df_attn_args* a, bool allow_split, bool pair) {
   Plan best{};
-  const int sms = sm_count_cached();
+  const int sms = pair ? sm_count_cached() / 2 : sm_count_cached();
   for (int i = 0; i < a->num_heads; ++i) best.ns[i] = 1;
   order_heads(a, best.ns, best.order);
-  double best_t = simulate(a, best.ns, best.order, sms);
+  double best_t = simulate(a, best.ns, best.order, sms, pair);
   if (allow_split) {
     int max_tiles = 1;
     for (int h = 0; h < a->num_heads; ++h) max_tiles = std::max(max_tiles, (a->heads[h].n_tok + 127) / 128);
@@ -628,7 +1102,7 @@ Plan make_plan(const df_attn_args* a, bool allow_split) {
         c.ns[h] = static_cast<uint8_t>(std::min(kMaxSplit, std::max(1, (tiles + cap - 1) / cap)));
       }
       order_heads(a, c.ns, c.order);
-      const double t = simulate(a, c.ns, c.order, sms);
+      const double t = simulate(a, c.ns, c.order, sms, pair);
       if (t < best_t * 0.995) {
         best_t = t;
         std::memcpy(best.ns, c.ns, sizeof(c.ns));
@@ -636,8 +1110,8 @@ Plan make_plan(const df_attn_args* a, bool allow_split) {
       }
     }
   }
-  best.ws_bytes = workspace_need(a, best.ns);
-  const int nq = (a->hw + 255) / 256;
+  best.ws_bytes = workspace_need(a, best.ns, pair);
+  const int nq = (a->hw + item_rows(pair) - 1) / item_rows(pair);
   best.n_items = 0;
   for (int h = 0; h < a->num_heads; ++h) best.n_items += nq * best.ns[h];
   return best;
@@ -654,12 +1128,13 @@ PlanCache& plan_cache() {
   return c;
 }
 
-Plan get_plan(const df_attn_args* a, bool allow_split) {
+Plan get_plan(const df_attn_args* a, bool allow_split, bool pair) {
   std::vector<int64_t> key;
-  key.reserve(a->num_heads + 4);
+  key.reserve(a->num_heads + 5);
   key.push_back(a->hw);
   key.push_back(a->head_dim);
   key.push_back(allow_split);
+  key.push_back(pair);
   key.push_back(sm_count_cached());
   for (int i = 0; i < a->num_heads; ++i) key.push_back(a->heads[i].n_tok);
   PlanCache& pc = plan_cache();
@@ -668,7 +1143,7 @@ Plan get_plan(const df_attn_args* a, bool allow_split) {
     auto it = pc.map.find(key);
     if (it != pc.map.end()) return it->second;
   }
-  Plan p = make_plan(a, allow_split);
+  Plan p = make_plan(a, allow_split, pair);
   std::lock_guard<std::mutex> g(pc.mu);
   if (pc.map.size() > 4096) pc.map.clear();
   pc.map.emplace(std::move(key), p);
@@ -704,14 +1179,20 @@ int validate(const df_attn_args* a) {
   return DF_OK;
 }
 
+// CTA-pair kernel: d = 128 only; DF_ATTN_SINGLE_CTA forces the 1-CTA kernel.
+bool use_pair(const df_attn_args* a) {
+  if (a->head_dim != 128 || (a->flags & DF_ATTN_SINGLE_CTA)) return false;
+  return (a->flags & DF_ATTN_PAIR) != 0;
+}
+
 }  // namespace
 
 extern "C" int df_attn_workspace_bytes(const df_attn_args* a, int64_t* bytes) {
   int rc = validate(a);
   if (rc != DF_OK) return rc;
   if (!bytes) return set_error(DF_E_ARG, "df_attn_workspace_bytes: null output");
-  const bool probe = (a->flags & DF_ATTN_PROBE) != 0;
-  *bytes = get_plan(a, !probe).ws_bytes;
+  const bool pair = use_pair(a);
+  *bytes = get_plan(a, (a->flags & DF_ATTN_PROBE) == 0 || pair, pair).ws_bytes;
   return DF_OK;
 }
 
@@ -723,22 +1204,23 @@ extern "C" int df_attn_fwd(const df_attn_args* a, void* stream) {
     return set_error(DF_E_ARG, "df_attn_fwd: probe epilogue needs region_of_slot, row_sampled, probe_rows");
 
   // Split plan; fall back to no splitting when the workspace cannot hold it.
-  Plan plan = get_plan(a, !probe);
+  const bool pair = use_pair(a);
+  Plan plan = get_plan(a, !probe || pair, pair);  // the 1-CTA probe epilogue does not combine pieces
   if (plan.ws_bytes > 0 && (!a->workspace || a->workspace_bytes < plan.ws_bytes ||
                             (reinterpret_cast<uintptr_t>(a->workspace) & 255)))
-    plan = get_plan(a, false);
+    plan = get_plan(a, false, pair);
 
   AttnParams p;
   std::memset(&p, 0, sizeof(p));
   rc = encode_rowmajor_bf16(&p.qmap, a->q, a->q_rows, a->head_dim);
   if (rc != DF_OK) return rc;
-  std::memcpy(p.kvmap, a->kv_maps, static_cast<size_t>(a->num_arenas) * 2 * DF_TMAP_BYTES);
+  std::memcpy(p.kvmap, a->kv_maps, static_cast<size_t>(a->num_arenas) * DF_MAPS_PER_ARENA * DF_TMAP_BYTES);
   p.out = static_cast<__nv_bfloat16*>(a->out);
   p.out_ld = a->out_ld;
   p.hw = a->hw;
   p.d_out = a->d_out;
   p.n_heads = a->num_heads;
-  p.n_qpairs = (a->hw + 2 * kBM - 1) / (2 * kBM);
+  p.n_qpairs = (a->hw + item_rows(pair) - 1) / item_rows(pair);
   p.max_slots = probe ? a->max_slots : 1;
   p.region_tab = a->region_of_slot;
   p.row_sampled = a->row_sampled;
@@ -763,11 +1245,12 @@ extern "C" int df_attn_fwd(const df_attn_args* a, void* stream) {
     }
   }
   if (groups) {
-    const int64_t cnt_bytes = ((groups * 4 + 255) / 256) * 256;
+    const int64_t ranks = pair ? 2 : 1;
+    const int64_t cnt_bytes = ((groups * ranks * 4 + 255) / 256) * 256;
     uint8_t* ws = static_cast<uint8_t*>(a->workspace);
     p.ws_cnt = reinterpret_cast<int32_t*>(ws);
     p.ws_o = reinterpret_cast<float*>(ws + cnt_bytes);
-    p.ws_ml = p.ws_o + slots * 2 * kBM * a->head_dim;
+    p.ws_ml = p.ws_o + slots * ranks * 2 * kBM * a->head_dim;
   }
   int acc = 0;
   for (int r = 0; r < a->num_heads; ++r) {
@@ -777,8 +1260,9 @@ extern "C" int df_attn_fwd(const df_attn_args* a, void* stream) {
   }
   p.item_prefix[a->num_heads] = acc;
 
-  const int grid = acc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (pair) return probe ? launch_attn_pair<true>(p, 2 * acc, s) : launch_attn_pair<false>(p, 2 * acc, s);
+  const int grid = acc;
   if (a->head_dim == 128)
     return probe ? launch_attn<128, true>(p, grid, s) : launch_attn<128, false>(p, grid, s);
   return probe ? launch_attn<64, true>(p, grid, s) : launch_attn<64, false>(p, grid, s);

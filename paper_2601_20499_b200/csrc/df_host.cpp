@@ -53,7 +53,7 @@ static EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-int encode_rowmajor_bf16(CUtensorMap* map, const void* base, int64_t rows, int32_t width) {
+int encode_rowmajor_bf16(CUtensorMap* map, const void* base, int64_t rows, int32_t width, int32_t box_rows) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return set_error(DF_E_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
   if (width != 64 && width != 128) return set_error(DF_E_SHAPE, "tensor map width %d not 64/128", width);
@@ -61,7 +61,7 @@ int encode_rowmajor_bf16(CUtensorMap* map, const void* base, int64_t rows, int32
   if (reinterpret_cast<uintptr_t>(base) & 15) return set_error(DF_E_ARG, "tensor map base not 16-byte aligned");
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(width), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(width) * 2};
-  cuuint32_t box[2] = {64, 128};
+  cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -123,10 +123,12 @@ extern "C" int df_device_check(int32_t* sm_count) {
 extern "C" int df_kv_arena_maps(const void* k_base, const void* v_base, int64_t rows, int32_t head_dim,
                                 uint8_t* out_maps) {
   if (!k_base || !v_base || !out_maps) return set_error(DF_E_ARG, "df_kv_arena_maps: null pointer");
-  CUtensorMap maps[2];
-  int rc = encode_rowmajor_bf16(&maps[0], k_base, rows, head_dim);
+  CUtensorMap maps[DF_MAPS_PER_ARENA];
+  int rc = encode_rowmajor_bf16(&maps[0], k_base, rows, head_dim, 128);
   if (rc != DF_OK) return rc;
-  rc = encode_rowmajor_bf16(&maps[1], v_base, rows, head_dim);
+  rc = encode_rowmajor_bf16(&maps[1], v_base, rows, head_dim, 128);
+  if (rc != DF_OK) return rc;
+  rc = encode_rowmajor_bf16(&maps[2], k_base, rows, head_dim, 64);  // K halves of the CTA-pair kernel
   if (rc != DF_OK) return rc;
   std::memcpy(out_maps, maps, sizeof(maps));
   return DF_OK;

@@ -14,7 +14,7 @@ int set_error(int code, const char* fmt, ...);
 int set_cuda_error(const char* what, cudaError_t e);
 
 // TMA descriptor for a row-major bf16 matrix [rows][width] (width 64 or 128),
-// box = 128 rows x 64 columns (128 bytes), SWIZZLE_128B, OOB -> zero.
-int encode_rowmajor_bf16(CUtensorMap* map, const void* base, int64_t rows, int32_t width);
+// box = box_rows rows x 64 columns (128 bytes), SWIZZLE_128B, OOB -> zero.
+int encode_rowmajor_bf16(CUtensorMap* map, const void* base, int64_t rows, int32_t width, int32_t box_rows = 128);
 
 }  // namespace dfb

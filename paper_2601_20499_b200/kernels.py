@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -16,6 +17,8 @@ from . import _lib
 from .errors import ShapeError
 
 TOKEN_ALIGN = 128  # head regions start on a kv-tile boundary
+# d = 128 launches use the CTA-pair kernel (cta_group::2) unless disabled here or per call.
+USE_CTA_PAIR = os.environ.get("DF_CTA_PAIR", "0") == "1"
 SUPPORTED_WIDTHS = (64, 128)
 
 
@@ -53,7 +56,7 @@ class KVArena:
         self.k = torch.zeros(total_rows, width, dtype=torch.bfloat16, device=self.device)
         self.v = torch.zeros(total_rows, width, dtype=torch.bfloat16, device=self.device)
         _lib.require_device(self.device.index if self.device.index is not None else torch.cuda.current_device())
-        buf = (ctypes.c_uint8 * (2 * _lib.DF_TMAP_BYTES))()
+        buf = (ctypes.c_uint8 * (_lib.DF_MAPS_PER_ARENA * _lib.DF_TMAP_BYTES))()
         _lib.call(
             "df_kv_arena_maps",
             ctypes.c_void_p(self.k.data_ptr()),
@@ -111,6 +114,7 @@ def attention(
     scale: float,
     probe: ProbeBuffers | None = None,
     stream: torch.cuda.Stream | None = None,
+    pair: bool | None = None,
 ) -> None:
     """One ragged launch over every head in ``work``.
 
@@ -136,7 +140,7 @@ def attention(
             sub_probe = None
             if probe is not None:
                 sub_probe = ProbeBuffers(probe.region_of_slot[sl], probe.row_sampled, probe.probe_rows[sl])
-            attention(q, out, work[sl], hw, scale, sub_probe, stream)
+            attention(q, out, work[sl], hw, scale, sub_probe, stream, pair)
         return
     if q.dtype != torch.bfloat16 or out.dtype != torch.bfloat16:
         raise ShapeError("q and out must be bfloat16")
@@ -180,8 +184,10 @@ def attention(
     args.num_arenas = len(arenas)
     args.heads = descs
     args.kv_maps = ctypes.cast(maps_buf, ctypes.c_void_p)
+    use_pair = USE_CTA_PAIR if pair is None else pair
+    args.flags = _lib.DF_ATTN_PAIR if use_pair else _lib.DF_ATTN_SINGLE_CTA
     if probe is not None:
-        args.flags = _lib.DF_ATTN_PROBE
+        args.flags |= _lib.DF_ATTN_PROBE
         args.max_slots = probe.region_of_slot.shape[1]
         args.region_of_slot = probe.region_of_slot.data_ptr()
         args.row_sampled = probe.row_sampled.data_ptr()

@@ -21,7 +21,8 @@ def _ref(q, k, v, scale):
     (64, 300, [40000, 300, 900]),    # split + unsplit heads in one launch, ragged tails
     (128, 200, [2000] * 40),         # many heads; last pair has a single valid tile
 ])
-def test_attention_matches_torch(width, hw, ctxs):
+@pytest.mark.parametrize("pair", [False, True])
+def test_attention_matches_torch(width, hw, ctxs, pair):
     from paper_2601_20499_b200 import kernels as K
 
     torch.manual_seed(0)
@@ -38,7 +39,7 @@ def test_attention_matches_torch(width, hw, ctxs):
         arena.v[base:base + c] = torch.randn(c, width, device=dev).to(torch.bfloat16)
         work.append(K.HeadWork(arena, base, c, h, h))
     scale = 1.0 / math.sqrt(width)
-    K.attention(q, out, work, hw, scale)
+    K.attention(q, out, work, hw, scale, pair=pair)
     torch.cuda.synchronize()
     for h, w in enumerate(work):
         ref = _ref(q[h * hw:(h + 1) * hw], arena.k[w.base_row:w.base_row + w.n_tok],
@@ -48,8 +49,9 @@ def test_attention_matches_torch(width, hw, ctxs):
         assert err <= 2e-2, (h, err)
 
 
+@pytest.mark.parametrize("pair", [False, True])
 @pytest.mark.parametrize("scale_q", [1.0, 6.0])
-def test_stale_rows_and_masked_tails(scale_q):
+def test_stale_rows_and_masked_tails(scale_q, pair):
     """Arena rows past each head's context hold stale finite data (as after an
     eviction): masked tail columns must contribute nothing, with both the MUFU
     and the polynomial exp2 paths; large logits exercise the lazy rescale."""
@@ -65,7 +67,7 @@ def test_stale_rows_and_masked_tails(scale_q):
     out = torch.full((len(ctxs) * hw, width), float("nan"), device=dev, dtype=torch.bfloat16)
     work = [K.HeadWork(arena, arena.allocate(c), c, h, h) for h, c in enumerate(ctxs)]
     scale = 1.0 / math.sqrt(width)
-    K.attention(q, out, work, hw, scale)
+    K.attention(q, out, work, hw, scale, pair=pair)
     torch.cuda.synchronize()
     assert not torch.isnan(out.float()).any()
     for h, w in enumerate(work):
