@@ -106,25 +106,35 @@ class ProbeBuffers:
     probe_rows: torch.Tensor  # float32 [heads, hw, 3]
 
 
-def attention(
+class PreparedLaunch:
+    """A fully built df_attn_fwd / df_kv_append call: launching is one C call."""
+
+    def __init__(self, fn: str, args: tuple, keep: tuple):
+        self.fn, self.args, self.keep = fn, args, keep
+
+    def launch(self, stream: torch.cuda.Stream | None = None) -> None:
+        _lib.call(self.fn, *self.args, _stream_handle(stream))
+
+
+def prepare_attention(
     q: torch.Tensor,
     out: torch.Tensor,
     work: list[HeadWork],
     hw: int,
     scale: float,
     probe: ProbeBuffers | None = None,
-    stream: torch.cuda.Stream | None = None,
     pair: bool | None = None,
-) -> None:
-    """One ragged launch over every head in ``work``.
+    stream: torch.cuda.Stream | None = None,
+) -> list[PreparedLaunch]:
+    """Build the launch(es) of one ragged attention over every head in ``work``.
 
     ``q``: bf16 [q_heads*hw, width] (width = arena width); ``out``: bf16
-    [o_heads*hw, d_out] with row stride ``out.stride(0)``.
+    [o_heads*hw, d_out] with row stride ``out.stride(0)``.  One launch carries
+    <= DF_MAX_HEADS heads from <= DF_MAX_ARENAS arenas; longer lists split into
+    contiguous runs (a session uses one arena: one launch).
     """
     if not work:
-        return
-    # One launch carries <= DF_MAX_HEADS heads from <= DF_MAX_ARENAS arenas;
-    # split contiguous runs otherwise (sessions use one arena: one launch).
+        return []
     chunks, cur, seen = [], [], set()
     for i, w in enumerate(work):
         new_arena = id(w.arena) not in seen
@@ -135,13 +145,14 @@ def attention(
         seen.add(id(w.arena))
     chunks.append(cur)
     if len(chunks) > 1:
+        out_launches = []
         for c in chunks:
             sl = slice(c[0], c[-1] + 1)
             sub_probe = None
             if probe is not None:
                 sub_probe = ProbeBuffers(probe.region_of_slot[sl], probe.row_sampled, probe.probe_rows[sl])
-            attention(q, out, work[sl], hw, scale, sub_probe, stream, pair)
-        return
+            out_launches += prepare_attention(q, out, work[sl], hw, scale, sub_probe, pair, stream)
+        return out_launches
     if q.dtype != torch.bfloat16 or out.dtype != torch.bfloat16:
         raise ShapeError("q and out must be bfloat16")
     if not q.is_cuda or not out.is_cuda:
@@ -160,8 +171,6 @@ def attention(
         a = idx.get(id(w.arena))
         if a is None:
             a = len(arenas)
-            if a >= _lib.DF_MAX_ARENAS:
-                raise ShapeError(f"more than {_lib.DF_MAX_ARENAS} KV arenas in one layer")
             idx[id(w.arena)] = a
             arenas.append(w.arena)
         descs[i].base_row = w.base_row
@@ -192,14 +201,29 @@ def attention(
         args.region_of_slot = probe.region_of_slot.data_ptr()
         args.row_sampled = probe.row_sampled.data_ptr()
         args.probe_rows = probe.probe_rows.data_ptr()
-    handle = _stream_handle(stream)
     need = ctypes.c_int64(0)
     _lib.call("df_attn_workspace_bytes", ctypes.byref(args), ctypes.byref(need))
+    ws = None
     if need.value > 0:
-        ws = _split_workspace(q.device, handle.value, need.value)
+        ws = _split_workspace(q.device, _stream_handle(stream).value, need.value)
         args.workspace = ws.data_ptr()
         args.workspace_bytes = ws.numel()
-    _lib.call("df_attn_fwd", ctypes.byref(args), handle)
+    return [PreparedLaunch("df_attn_fwd", (ctypes.byref(args),), (args, descs, maps_buf, ws, q, out, probe))]
+
+
+def attention(
+    q: torch.Tensor,
+    out: torch.Tensor,
+    work: list[HeadWork],
+    hw: int,
+    scale: float,
+    probe: ProbeBuffers | None = None,
+    stream: torch.cuda.Stream | None = None,
+    pair: bool | None = None,
+) -> None:
+    """Ragged attention over every head in ``work`` (see prepare_attention)."""
+    for launch in prepare_attention(q, out, work, hw, scale, probe, pair, stream):
+        launch.launch(stream)
 
 
 _WORKSPACES: dict[tuple[int, int], torch.Tensor] = {}
@@ -219,14 +243,22 @@ def _split_workspace(device: torch.device, stream_handle: int, nbytes: int) -> t
     return ws
 
 
-def copy_segments(segs: list[tuple[int, int, int, int, int, int]], stream: torch.cuda.Stream | None = None) -> None:
-    """Batched 16-byte-vectorised device copies, (src, dst, rows, src_ld, dst_ld, row_bytes) each."""
+def prepare_copies(segs: list[tuple[int, int, int, int, int, int]]) -> list[PreparedLaunch]:
+    """df_kv_append launches (<= DF_MAX_APPEND_SEGS segments each), built ahead of time."""
+    out = []
     for i in range(0, len(segs), _lib.DF_MAX_APPEND_SEGS):
         chunk = segs[i : i + _lib.DF_MAX_APPEND_SEGS]
         arr = (_lib.CopySeg * len(chunk))()
         for j, s in enumerate(chunk):
             arr[j].src, arr[j].dst, arr[j].rows, arr[j].src_ld, arr[j].dst_ld, arr[j].row_bytes = s
-        _lib.call("df_kv_append", arr, ctypes.c_int32(len(chunk)), _stream_handle(stream))
+        out.append(PreparedLaunch("df_kv_append", (arr, ctypes.c_int32(len(chunk))), (arr,)))
+    return out
+
+
+def copy_segments(segs: list[tuple[int, int, int, int, int, int]], stream: torch.cuda.Stream | None = None) -> None:
+    """Batched 16-byte-vectorised device copies, (src, dst, rows, src_ld, dst_ld, row_bytes) each."""
+    for launch in prepare_copies(segs):
+        launch.launch(stream)
 
 
 class PackPlan:
