@@ -86,8 +86,14 @@ struct __align__(64) AttnParams {
 
 template <int D>
 struct AttnCfg {
-  static constexpr int kStagesK = 2;
-  static constexpr int kStagesV = (D == 128) ? 2 : 3;
+#ifndef DF_STAGES_K128
+#define DF_STAGES_K128 2
+#endif
+#ifndef DF_STAGES_V128
+#define DF_STAGES_V128 2
+#endif
+  static constexpr int kStagesK = (D == 128) ? DF_STAGES_K128 : 2;
+  static constexpr int kStagesV = (D == 128) ? DF_STAGES_V128 : 3;
   static constexpr int kBoxes = D / 64;                 // 128-byte wide TMA boxes per row
   static constexpr int kTileBytes = kBN * D * 2;        // one [128 x D] bf16 tile
   static constexpr int kBoxBytes = kBN * 128;           // one [128 x 64] box
