@@ -373,6 +373,54 @@ class LayerTrace:
     macs: int
 
 
+class ToyModel:
+    """scenario.py:70-120 (ToyModel): seeded q/k/v/o projections, x @ W per head, residual mix.
+
+    ``frame_input`` = frame(i) + 0.1 * jitter(i, t) (scenario.py:95-101, DENOISE_JITTER);
+    ``qkv`` splits x @ W into (heads, HW, head_dim) (scenario.py:102-114); ``mix`` merges the
+    head outputs to (HW, heads*head_dim) and applies W_o (scenario.py:116-120).
+    """
+
+    DENOISE_JITTER = 0.1
+
+    def __init__(self, num_layers: int, num_heads: int, head_dim: int, HW: int, seed: int, weight_scale: float = 1.0):
+        self.num_layers, self.num_heads, self.head_dim, self.HW, self.seed = num_layers, num_heads, head_dim, HW, seed
+        D = num_heads * head_dim
+        scale = weight_scale / math.sqrt(D)
+        self.weights = [{n: matrix(derive(seed, f"w{n}", layer), D, D, scale) for n in ("q", "k", "v", "o")}
+                        for layer in range(num_layers)]
+
+    @property
+    def model_dim(self) -> int:
+        return self.num_heads * self.head_dim
+
+    def frame_input(self, i: int, t: int) -> np.ndarray:
+        base = matrix(derive(self.seed, "frame", i), self.HW, self.model_dim)
+        jitter = matrix(derive(self.seed, "denoise", i, t), self.HW, self.model_dim)
+        return base + self.DENOISE_JITTER * jitter
+
+    def qkv(self, layer: int, x: np.ndarray, i: int, t: int):
+        w = self.weights[layer]
+        return tuple((x @ w[n]).reshape(self.HW, self.num_heads, self.head_dim).transpose(1, 0, 2)
+                     for n in ("q", "k", "v"))
+
+    def mix(self, layer: int, outputs: np.ndarray) -> np.ndarray:
+        merged = outputs.transpose(1, 0, 2).reshape(self.HW, self.model_dim)
+        return merged @ self.weights[layer]["o"]
+
+
+def array_digest(*arrays) -> str:
+    """container.py:30-37: sha256 over (shape, little-endian bytes) of each array."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h.update(str(a.shape).encode())
+        h.update(a.astype(a.dtype.newbyteorder("<"), copy=False).tobytes())
+    return h.hexdigest()
+
+
 @dataclass
 class OracleRun:
     classes: list[int] | None = None
@@ -383,10 +431,11 @@ class OracleRun:
     step_macs: list[int] = field(default_factory=list)
     cache_ratio: float = 1.0
     traces: list[LayerTrace] = field(default_factory=list)
+    frames: list[np.ndarray] = field(default_factory=list)  # x after the last denoise iteration, per AR step
 
 
 def run_session(model, cfg: Config, mode: str, keep_traces: bool = False, qkv_hook=None) -> OracleRun:
-    """engine.py:268-476 at frame-id + fp64 numerics level (open-loop models).
+    """engine.py:268-476 at frame-id + fp64 numerics level (open- and closed-loop models).
 
     ``qkv_hook(layer, ar, t, q, k, v)`` may replace the model's Q/K/V (used to
     feed the oracle the same bf16-rounded inputs as the device).
@@ -431,7 +480,9 @@ def run_session(model, cfg: Config, mode: str, keep_traces: bool = False, qkv_ho
                         captured.append((layer, h, q[h].copy(), ck[h], region_kinds(ids[layer][h], pol[layer][h])))
                 if keep_traces:
                     run.traces.append(LayerTrace(i, t, layer, q, k, v, out, frames, nc, m))
-                model.mix(layer, out)
+                m = model.mix(layer, out)
+                if m is not None and x is not None:
+                    x = x + m  # engine.py:443 residual (closed-loop models)
         if classify_at is not None and run.classes is None and i == classify_at[0]:
             F = np.zeros((cfg.total_heads, 3))
             for layer, h, qh, keys, kinds in captured:
@@ -450,7 +501,9 @@ def run_session(model, cfg: Config, mode: str, keep_traces: bool = False, qkv_ho
             for h in range(H):
                 data[(layer, h, i)] = (k[h], v[h])
                 ids[layer][h] = append(ids[layer][h], i, pol[layer][h])
-        run.frame_ids_after_step.append([[list(x) for x in lay] for lay in ids])
+        if x is not None:
+            run.frames.append(x)
+        run.frame_ids_after_step.append([[list(f) for f in lay] for lay in ids])
         run.kernel_calls_steady = calls
         run.step_macs.append(macs)
     return run
