@@ -31,6 +31,14 @@
  *                      objective sum)
  *   df_kv_arena_maps   (no reference counterpart: builds the TMA descriptors of
  *                      a device KV arena once per allocation)
+ *   df_qkv_project     scenario.py:102-114 ToyModel.qkv (x @ W_q|k|v, split
+ *                      into heads) + engine.py:423-426 FrameBlock wrap: the
+ *                      epilogue writes Q in the FMHA layout and the current
+ *                      K/V straight into each head's pending ring slot, so no
+ *                      append/staging copy remains
+ *   df_out_project     scenario.py:116-120 ToyModel.mix (merge heads, @ W_o)
+ *                      + engine.py:443 residual x = x + mix(...), fused into
+ *                      one GEMM epilogue
  */
 #ifndef DF_B200_H
 #define DF_B200_H
@@ -150,6 +158,30 @@ DF_API int df_greedy_classify(const double* F, int64_t total_heads, int64_t n_du
                        int8_t* classes_out, double* objective_out);
 
 /* ---- misc ---- */
+/* ---- fused projections (tcgen05 GEMM, persistent, bf16 in / fp32 accumulate) */
+typedef struct df_qkv_args {
+  const void* x;        /* bf16 [hw, in_dim] row-major: the layer input             */
+  const void* w_qkv;    /* bf16 [3*num_heads*head_dim, in_dim]: rows = the columns of
+                           W_q, then W_k, then W_v of these heads ([W_q|W_k|W_v]^T)  */
+  int32_t hw, num_heads, head_dim;  /* head_dim 64 or 128                          */
+  int32_t in_dim;       /* multiple of 8 (16-byte rows)                             */
+  void* q_out;          /* bf16 [num_heads*hw, head_dim] (df_attn_fwd's q)           */
+  void* k_dst[DF_MAX_HEADS]; /* bf16 row 0 of each head's destination K block       */
+  void* v_dst[DF_MAX_HEADS]; /* (the pending ring slot), rows strided by kv_ld      */
+  int64_t kv_ld;        /* elements between consecutive K/V rows (arena width)      */
+} df_qkv_args;
+DF_API int df_qkv_project(const df_qkv_args* args, void* stream);
+
+typedef struct df_oproj_args {
+  const void* o;        /* bf16 [num_heads*hw, head_dim]: df_attn_fwd's output     */
+  const void* w_o;      /* bf16 [out_dim, num_heads*head_dim]: rows = columns of W_o */
+  int32_t hw, num_heads, head_dim;
+  int32_t out_dim;      /* multiple of 32                                           */
+  float* x;             /* fp32 [hw, out_dim], updated in place: x += merge(o)@W_o  */
+  void* x_bf16;         /* bf16 [hw, out_dim] copy of the updated x, or NULL        */
+} df_oproj_args;
+DF_API int df_out_project(const df_oproj_args* args, void* stream);
+
 DF_API const char* df_last_error(void);
 DF_API int df_version(void);
 /* DF_OK when a compute-capability-10.x device is visible. */

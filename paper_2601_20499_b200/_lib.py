@@ -90,6 +90,34 @@ class CopySeg(ctypes.Structure):
     ]
 
 
+class QkvArgs(ctypes.Structure):
+    _fields_ = [
+        ("x", ctypes.c_void_p),
+        ("w_qkv", ctypes.c_void_p),
+        ("hw", ctypes.c_int32),
+        ("num_heads", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32),
+        ("in_dim", ctypes.c_int32),
+        ("q_out", ctypes.c_void_p),
+        ("k_dst", ctypes.c_void_p * DF_MAX_HEADS),
+        ("v_dst", ctypes.c_void_p * DF_MAX_HEADS),
+        ("kv_ld", ctypes.c_int64),
+    ]
+
+
+class OprojArgs(ctypes.Structure):
+    _fields_ = [
+        ("o", ctypes.c_void_p),
+        ("w_o", ctypes.c_void_p),
+        ("hw", ctypes.c_int32),
+        ("num_heads", ctypes.c_int32),
+        ("head_dim", ctypes.c_int32),
+        ("out_dim", ctypes.c_int32),
+        ("x", ctypes.c_void_p),
+        ("x_bf16", ctypes.c_void_p),
+    ]
+
+
 # Every symbol include/df_b200.h declares, with its ctypes signature.
 _SIGNATURES = {
     "df_attn_fwd": (ctypes.c_int, [ctypes.POINTER(AttnArgs), ctypes.c_void_p]),
@@ -121,6 +149,8 @@ _SIGNATURES = {
             ctypes.POINTER(ctypes.c_double),
         ],
     ),
+    "df_qkv_project": (ctypes.c_int, [ctypes.POINTER(QkvArgs), ctypes.c_void_p]),
+    "df_out_project": (ctypes.c_int, [ctypes.POINTER(OprojArgs), ctypes.c_void_p]),
     "df_last_error": (ctypes.c_char_p, []),
     "df_version": (ctypes.c_int, []),
     "df_device_check": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int32)]),

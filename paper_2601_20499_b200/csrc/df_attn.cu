@@ -1003,6 +1003,17 @@ static int launch_attn(const AttnParams& p, int grid, cudaStream_t stream) {
   return DF_OK;
 }
 
+int sm_count_cached() {
+  static int count = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev);
+    if (count <= 0) count = 148;
+  });
+  return count;
+}
+
 }  // namespace dfb
 
 using namespace dfb;
@@ -1028,16 +1039,6 @@ struct Plan {
   int n_items;
 };
 
-int sm_count_cached() {
-  static int count = 0;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev);
-    if (count <= 0) count = 148;
-  });
-  return count;
-}
 
 // rows of one work item: a pair of 128-row tiles, or 2 x 256 rows for the CTA-pair kernel
 inline int item_rows(bool pair) { return pair ? 512 : 256; }

@@ -53,14 +53,17 @@ static EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
-int encode_rowmajor_bf16(CUtensorMap* map, const void* base, int64_t rows, int32_t width, int32_t box_rows) {
+int encode_bf16_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int32_t box_rows) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return set_error(DF_E_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
-  if (width != 64 && width != 128) return set_error(DF_E_SHAPE, "tensor map width %d not 64/128", width);
+  if (cols < 64 || cols % 8 || ld < cols || ld % 8)
+    return set_error(DF_E_SHAPE, "tensor map cols %lld / ld %lld (need >= 64, multiples of 8)", (long long)cols,
+                     (long long)ld);
   if (rows < 1 || rows > (int64_t(1) << 31)) return set_error(DF_E_SHAPE, "tensor map rows %lld", (long long)rows);
+  if (box_rows < 1 || box_rows > 256) return set_error(DF_E_SHAPE, "tensor map box rows %d", box_rows);
   if (reinterpret_cast<uintptr_t>(base) & 15) return set_error(DF_E_ARG, "tensor map base not 16-byte aligned");
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(width), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(width) * 2};
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
   cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
@@ -68,6 +71,11 @@ int encode_rowmajor_bf16(CUtensorMap* map, const void* base, int64_t rows, int32
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(DF_E_CUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", int(r));
   return DF_OK;
+}
+
+int encode_rowmajor_bf16(CUtensorMap* map, const void* base, int64_t rows, int32_t width, int32_t box_rows) {
+  if (width != 64 && width != 128) return set_error(DF_E_SHAPE, "tensor map width %d not 64/128", width);
+  return encode_bf16_2d(map, base, rows, width, width, box_rows);
 }
 
 // numpy's float64 add.reduce of a contiguous 1-D array is one pairwise_sum

@@ -1,0 +1,371 @@
+// df_proj.cu -- the two projection GEMMs around the attention launch of a
+// Dummy Forcing layer, on the 5th-gen tensor cores (sm_100a), with the data
+// movement the reference does afterwards fused into the epilogue.
+//
+//   df_qkv_project  [q|k|v] = x @ [W_q|W_k|W_v]   (scenario.py:102-114)
+//                   epilogue: Q -> (head, row) layout read by df_attn_fwd,
+//                   K/V -> each head's pending ring slot (engine.py:423-426
+//                   FrameBlock + the append copy of kv_cache.py:177-185).
+//   df_out_project  x += merge(o) @ W_o            (scenario.py:116-120 and
+//                   the residual of engine.py:443); A is read per head
+//                   straight from the FMHA output, so the head merge
+//                   (transpose) costs nothing.
+//
+// Persistent kernel, one CTA per SM, 192 threads:
+//   warp 0      TMA producer: [128 x 64] A box + [BN x 64] B box per stage
+//               (SWIZZLE_128B), kStages-deep ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer,
+//               accumulators double-buffered in TMEM (2 x BN fp32 columns)
+//   warps 2-5   epilogue: tcgen05.ld 32 columns at a time, fused stores,
+//               overlapping the next tile's main loop
+// Tiles are walked m-fastest so consecutive CTAs share the same W tile in L2.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+
+#include "df_b200.h"
+#include "df_internal.h"
+#include "df_ptx.cuh"
+
+namespace dfb {
+namespace {
+
+constexpr int kPBM = 128;
+constexpr int kPBK = 64;  // one 128-byte swizzle atom of bf16 per stage
+constexpr int kPThreads = 192;
+
+enum { kEpiQKV = 0, kEpiOut = 1 };
+
+template <int BN>
+struct ProjCfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kABytes = kPBM * kPBK * 2;
+  static constexpr int kBBytes = BN * kPBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBarOff = kStages * kStageBytes;
+  static constexpr int kSmem = kBarOff + (2 * kStages + 4) * 8 + 16 + 1024;
+  static constexpr int kTmemCols = 2 * BN;
+};
+
+struct ProjParams {
+  CUtensorMap amap;
+  CUtensorMap bmap;
+  int32_t m, n, kblocks;
+  int32_t m_tiles, tiles;
+  int32_t a_cols;        // A column extent before the next head chunk starts
+  int32_t a_chunk_rows;  // row offset between consecutive A column chunks
+  int32_t hw, head_dim;
+  int32_t qkv_cols;  // num_heads * head_dim (QKV epilogue)
+  int32_t out_ld;    // x row stride (out-projection epilogue)
+  __nv_bfloat16* q_out;
+  __nv_bfloat16* k_dst[DF_MAX_HEADS];
+  __nv_bfloat16* v_dst[DF_MAX_HEADS];
+  int64_t kv_ld;
+  float* x;
+  __nv_bfloat16* x_bf16;
+};
+
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* f) {
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint4 v;
+    v.x = pack_bf16x2(f[8 * i + 0], f[8 * i + 1]);
+    v.y = pack_bf16x2(f[8 * i + 2], f[8 * i + 3]);
+    v.z = pack_bf16x2(f[8 * i + 4], f[8 * i + 5]);
+    v.w = pack_bf16x2(f[8 * i + 6], f[8 * i + 7]);
+    d4[i] = v;
+  }
+}
+
+template <int kEpi>
+__device__ __forceinline__ void epilogue_chunk(const ProjParams& p, int row, int n0, const uint32_t* r) {
+  float f[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(r[i]);
+  if constexpr (kEpi == kEpiQKV) {
+    const int which = n0 / p.qkv_cols;  // 0 q, 1 k, 2 v
+    const int rem = n0 - which * p.qkv_cols;
+    const int h = rem / p.head_dim;
+    const int col = rem - h * p.head_dim;
+    __nv_bfloat16* dst;
+    if (which == 0)
+      dst = p.q_out + (static_cast<int64_t>(h) * p.hw + row) * p.head_dim + col;
+    else
+      dst = (which == 1 ? p.k_dst[h] : p.v_dst[h]) + static_cast<int64_t>(row) * p.kv_ld + col;
+    store_bf16x32(dst, f);
+  } else {
+    float4* x4 = reinterpret_cast<float4*>(p.x + static_cast<int64_t>(row) * p.out_ld + n0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float4 a = x4[i];
+      a.x += f[4 * i + 0];
+      a.y += f[4 * i + 1];
+      a.z += f[4 * i + 2];
+      a.w += f[4 * i + 3];
+      x4[i] = a;
+      f[4 * i + 0] = a.x;
+      f[4 * i + 1] = a.y;
+      f[4 * i + 2] = a.z;
+      f[4 * i + 3] = a.w;
+    }
+    if (p.x_bf16) store_bf16x32(p.x_bf16 + static_cast<int64_t>(row) * p.out_ld + n0, f);
+  }
+}
+
+template <int BN, int kEpi>
+__global__ void __launch_bounds__(kPThreads, 1) df_proj_kernel(const __grid_constant__ ProjParams p) {
+  using C = ProjCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* acc_full = empty + C::kStages;  // [2]
+  uint64_t* acc_empty = acc_full + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(acc_full + a, 1);
+      mbar_init(acc_empty + a, 4);  // one arrive per epilogue warp
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      prefetch_tmap(&p.amap);
+      prefetch_tmap(&p.bmap);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+        const int mb = tile % p.m_tiles;
+        const int nb = tile / p.m_tiles;
+        for (int kb = 0; kb < p.kblocks; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          mbar_expect_tx(full + stage, C::kStageBytes);
+          const int kk = kb * kPBK;
+          const int chunk = kk / p.a_cols;
+          uint8_t* sa = smem + stage * C::kStageBytes;
+          tma_load_2d(sa, &p.amap, full + stage, kk - chunk * p.a_cols, mb * kPBM + chunk * p.a_chunk_rows);
+          tma_load_2d(sa + C::kABytes, &p.bmap, full + stage, kk, nb * BN);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(kPBM, BN, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+        mbar_wait(acc_empty + acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < p.kblocks; ++kb) {
+          mbar_wait(full + stage, phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
+          const uint32_t sb = sa + C::kABytes;
+#pragma unroll
+          for (int k = 0; k < kPBK / 16; ++k)
+            umma_ss(d, sdesc_sw128(sa + k * 32, 16, 1024), sdesc_sw128(sb + k * 32, 16, 1024), idesc,
+                    (kb | k) != 0);
+          umma_commit(empty + stage);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(acc_full + acc);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int quad = warp & 3;  // TMEM lanes 32*quad .. 32*quad+31
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
+      const int mb = tile % p.m_tiles;
+      const int nb = tile / p.m_tiles;
+      mbar_wait(acc_full + acc, acc_phase);
+      tc_fence_after();
+      const int row = mb * kPBM + quad * 32 + lane;
+      const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(quad * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(taddr + c * 32, r);
+        tmem_wait_ld();
+        const int n0 = nb * BN + c * 32;
+        if (row < p.m && n0 < p.n) epilogue_chunk<kEpi>(p, row, n0, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty + acc);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::kTmemCols);
+  }
+}
+
+template <int BN, int kEpi>
+int launch_proj(const ProjParams& p, int grid, cudaStream_t stream) {
+  auto kern = df_proj_kernel<BN, kEpi>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ProjCfg<BN>::kSmem);
+    if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(df_proj_kernel)", e);
+    configured = true;
+  }
+  kern<<<grid, kPThreads, ProjCfg<BN>::kSmem, stream>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error("df_proj_kernel launch", e);
+  return DF_OK;
+}
+
+// Tile width: fewest tensor-pipe "tile-columns" over whole waves of the
+// persistent grid (N=128 tiles pay ~6% more per FLOP than N=256 ones).
+int pick_bn(int64_t m, int64_t n) {
+  if (const char* env = std::getenv("DF_PROJ_BN")) {
+    const int v = std::atoi(env);
+    if (v == 128 || v == 256) return v;
+  }
+  const int64_t sms = sm_count_cached();
+  const int64_t mt = (m + kPBM - 1) / kPBM;
+  double best = 1e300;
+  int bn = 128;
+  for (int cand : {256, 128}) {
+    const int64_t tiles = mt * ((n + cand - 1) / cand);
+    const int64_t waves = (tiles + sms - 1) / sms;
+    const double cost = double(waves) * cand * (cand == 128 ? 1.06 : 1.0);
+    if (cost < best) {
+      best = cost;
+      bn = cand;
+    }
+  }
+  return bn;
+}
+
+bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
+
+int check_dims(const char* fn, int32_t hw, int32_t heads, int32_t d) {
+  if (hw < 1) return set_error(DF_E_SHAPE, "%s: hw %d < 1", fn, hw);
+  if (heads < 1 || heads > DF_MAX_HEADS)
+    return set_error(DF_E_SHAPE, "%s: num_heads %d outside [1, %d]", fn, heads, DF_MAX_HEADS);
+  if (d != 64 && d != 128) return set_error(DF_E_SHAPE, "%s: head_dim %d not 64 or 128", fn, d);
+  return DF_OK;
+}
+
+}  // namespace
+}  // namespace dfb
+
+using namespace dfb;
+
+extern "C" int df_qkv_project(const df_qkv_args* a, void* stream) {
+  if (!a || !a->x || !a->w_qkv || !a->q_out) return set_error(DF_E_ARG, "df_qkv_project: null argument");
+  int rc = check_dims("df_qkv_project", a->hw, a->num_heads, a->head_dim);
+  if (rc != DF_OK) return rc;
+  if (a->in_dim < 8 || a->in_dim % 8) return set_error(DF_E_SHAPE, "df_qkv_project: in_dim %d not a multiple of 8", a->in_dim);
+  if (a->kv_ld < a->head_dim || a->kv_ld % 8)
+    return set_error(DF_E_SHAPE, "df_qkv_project: kv_ld %lld (head_dim %d)", (long long)a->kv_ld, a->head_dim);
+  if (!aligned16(a->q_out)) return set_error(DF_E_ARG, "df_qkv_project: q_out not 16-byte aligned");
+  ProjParams p;
+  std::memset(&p, 0, sizeof(p));
+  for (int h = 0; h < a->num_heads; ++h) {
+    if (!a->k_dst[h] || !a->v_dst[h] || !aligned16(a->k_dst[h]) || !aligned16(a->v_dst[h]))
+      return set_error(DF_E_ARG, "df_qkv_project: head %d K/V destination null or not 16-byte aligned", h);
+    p.k_dst[h] = static_cast<__nv_bfloat16*>(a->k_dst[h]);
+    p.v_dst[h] = static_cast<__nv_bfloat16*>(a->v_dst[h]);
+  }
+  const int32_t cols = a->num_heads * a->head_dim;
+  p.m = a->hw;
+  p.n = 3 * cols;
+  p.kblocks = (a->in_dim + kPBK - 1) / kPBK;
+  p.a_cols = p.kblocks * kPBK;  // one chunk: A is x itself
+  p.a_chunk_rows = 0;
+  p.hw = a->hw;
+  p.head_dim = a->head_dim;
+  p.qkv_cols = cols;
+  p.q_out = static_cast<__nv_bfloat16*>(a->q_out);
+  p.kv_ld = a->kv_ld;
+  const int bn = pick_bn(p.m, p.n);
+  rc = encode_bf16_2d(&p.amap, a->x, a->hw, a->in_dim, a->in_dim, kPBM);
+  if (rc != DF_OK) return rc;
+  rc = encode_bf16_2d(&p.bmap, a->w_qkv, int64_t(p.n), a->in_dim, a->in_dim, bn);
+  if (rc != DF_OK) return rc;
+  p.m_tiles = (p.m + kPBM - 1) / kPBM;
+  p.tiles = p.m_tiles * ((p.n + bn - 1) / bn);
+  const int grid = p.tiles < sm_count_cached() ? p.tiles : sm_count_cached();
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return bn == 256 ? launch_proj<256, kEpiQKV>(p, grid, s) : launch_proj<128, kEpiQKV>(p, grid, s);
+}
+
+extern "C" int df_out_project(const df_oproj_args* a, void* stream) {
+  if (!a || !a->o || !a->w_o || !a->x) return set_error(DF_E_ARG, "df_out_project: null argument");
+  int rc = check_dims("df_out_project", a->hw, a->num_heads, a->head_dim);
+  if (rc != DF_OK) return rc;
+  if (a->out_dim < 32 || a->out_dim % 32)
+    return set_error(DF_E_SHAPE, "df_out_project: out_dim %d not a multiple of 32", a->out_dim);
+  if (!aligned16(a->x) || (a->x_bf16 && !aligned16(a->x_bf16)))
+    return set_error(DF_E_ARG, "df_out_project: x / x_bf16 not 16-byte aligned");
+  ProjParams p;
+  std::memset(&p, 0, sizeof(p));
+  const int32_t kdim = a->num_heads * a->head_dim;
+  p.m = a->hw;
+  p.n = a->out_dim;
+  p.kblocks = kdim / kPBK;
+  p.a_cols = a->head_dim;  // K index h*d + c lives in row h*hw + m, column c of the FMHA output
+  p.a_chunk_rows = a->hw;
+  p.hw = a->hw;
+  p.head_dim = a->head_dim;
+  p.out_ld = a->out_dim;
+  p.x = a->x;
+  p.x_bf16 = static_cast<__nv_bfloat16*>(a->x_bf16);
+  const int bn = pick_bn(p.m, p.n);
+  rc = encode_bf16_2d(&p.amap, a->o, int64_t(a->num_heads) * a->hw, a->head_dim, a->head_dim, kPBM);
+  if (rc != DF_OK) return rc;
+  rc = encode_bf16_2d(&p.bmap, a->w_o, a->out_dim, kdim, kdim, bn);
+  if (rc != DF_OK) return rc;
+  p.m_tiles = (p.m + kPBM - 1) / kPBM;
+  p.tiles = p.m_tiles * ((p.n + bn - 1) / bn);
+  const int grid = p.tiles < sm_count_cached() ? p.tiles : sm_count_cached();
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return bn == 256 ? launch_proj<256, kEpiOut>(p, grid, s) : launch_proj<128, kEpiOut>(p, grid, s);
+}

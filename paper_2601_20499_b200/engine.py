@@ -467,6 +467,36 @@ class Session:
             q, k, v = q[r.start : r.stop], k[r.start : r.stop], v[r.start : r.stop]
         return as_device_bf16(q, self.device), as_device_bf16(k, self.device), as_device_bf16(v, self.device)
 
+    def _project(self, layer, x, ar, t):
+        """(q, current blocks) of one layer.
+
+        A model with ``qkv_into`` (projection.ProjectedModel) writes K/V of the
+        current frame straight into the pending ring slots (df_qkv_project), so
+        the blocks are views of the ring and staging/append move nothing.
+        """
+        into = getattr(self.model, "qkv_into", None)
+        if into is None:
+            q, k, v = self._model_qkv(layer, x, ar, t)
+            return q, [FrameBlock(ar, k[h], v[h]) for h in range(k.shape[0])]
+        cfg = self.config
+        caches = self.caches[layer]
+        views = [c.pending_view(cfg.HW, cfg.head_dim, self.device) for c in caches]
+        q = torch.empty(len(caches), cfg.HW, cfg.head_dim, dtype=torch.bfloat16, device=self.device)
+        into(layer, x, ar, t, q, [kv[0] for kv in views], [kv[1] for kv in views], heads=self.head_range,
+             stream=self.stream)
+        return q, [FrameBlock(ar, k, v) for k, v in views]
+
+    def _mix(self, layer, outputs, x):
+        """engine.py:443: x = x + mix(outputs); fused in-place for models with ``mix_into``."""
+        gathered = self._gather_outputs(layer, outputs)
+        into = getattr(self.model, "mix_into", None)
+        if into is not None:
+            return into(layer, gathered, x, stream=self.stream)
+        m = self.model.mix(layer, gathered)
+        if m is None:
+            return x
+        return m if x is None else x + m
+
     def _run_step(self, ar_step: int) -> None:
         cfg = self.config
         final_kv = []
@@ -479,8 +509,7 @@ class Session:
             probes: dict[float, list[ProbeRequest]] = {r: [] for r in ratios}
             counters = StepCounters()
             for layer in range(cfg.num_layers):
-                q, k, v = self._model_qkv(layer, x, ar_step, t)
-                blocks = [FrameBlock(ar_step, k[h], v[h]) for h in range(k.shape[0])]
+                q, blocks = self._project(layer, x, ar_step, t)
                 pr = None
                 if ratios:
                     pr = self._probe_buffers(ratios[0])
@@ -495,9 +524,7 @@ class Session:
                     self._notify(ar_step, t, layer, q, outputs, blocks)
                 if final:
                     final_kv.append(blocks)
-                m = self.model.mix(layer, self._gather_outputs(layer, outputs))
-                if m is not None:
-                    x = m if x is None else x + m
+                x = self._mix(layer, outputs, x)
             for r in ratios:
                 self._finalize_probe((ar_step, t), r, probes[r])
             step_counters.append(counters)
@@ -512,7 +539,7 @@ class Session:
                     segs += self.shadow_caches[layer][h].append_segments(block, self.device)
         if segs:
             launch_segments(segs, s)
-        self._frames.append(x)
+        self._frames.append(getattr(x, "f32", x))
         self._step_counters.append((ar_step, step_counters))
         self._kernel_calls_last = list(step_counters[-1].kernel_calls)
         self._phys_last = [lc.physical_launches for lc in step_counters[-1].layers]
@@ -553,13 +580,10 @@ class Session:
             counters = StepCounters()
             x = self.model.frame_input(ar_step, t)
             for layer in range(cfg.num_layers):
-                q, k, v = self._model_qkv(layer, x, ar_step, t)
-                blocks = [FrameBlock(ar_step, k[h], v[h]) for h in range(k.shape[0])]
+                q, blocks = self._project(layer, x, ar_step, t)
                 outputs, lc = self._layer_attention(layer, q, self.caches[layer], blocks)
                 counters.add_layer(lc)
-                m = self.model.mix(layer, self._gather_outputs(layer, outputs))
-                if m is not None:
-                    x = m if x is None else x + m
+                x = self._mix(layer, outputs, x)
             walls.append(counters.wall_time_ns)
         walls.sort()
         mid = len(walls) // 2

@@ -304,3 +304,76 @@ def scores_finalize(probe: ProbeBuffers, stream: torch.cuda.Stream | None = None
         _stream_handle(stream),
     )
     return F
+
+
+# ------------------------------------------------------------ fused projections
+def _bf16_rows(t: torch.Tensor, name: str, cols: int | None = None) -> None:
+    if t.dtype != torch.bfloat16 or not t.is_cuda:
+        raise ShapeError(f"{name} must be a bf16 CUDA tensor, got {t.dtype} on {t.device}")
+    if t.dim() != 2 or t.stride(1) != 1 or (cols is not None and t.shape[1] != cols):
+        raise ShapeError(f"{name} must be a row-major 2-D matrix{'' if cols is None else f' with {cols} columns'}, "
+                         f"got shape {tuple(t.shape)} strides {t.stride()}")
+
+
+def prepare_qkv_projection(x: torch.Tensor, w_qkv: torch.Tensor, q_out: torch.Tensor, k_dst: list[torch.Tensor],
+                           v_dst: list[torch.Tensor], head_dim: int) -> PreparedLaunch:
+    """df_qkv_project: ``[q|k|v] = x @ [W_q|W_k|W_v]`` (scenario.py:102-114), fused scatter.
+
+    ``x`` bf16 [hw, in_dim]; ``w_qkv`` bf16 [3*heads*head_dim, in_dim] (the
+    transposed, concatenated projection weights of the heads); ``q_out`` bf16
+    [heads, hw, head_dim] contiguous; ``k_dst[h]`` / ``v_dst[h]`` bf16 [hw,
+    head_dim] row-strided views (the heads' pending ring slots) sharing one row
+    stride.
+    """
+    heads = len(k_dst)
+    if heads != len(v_dst) or not 1 <= heads <= _lib.DF_MAX_HEADS:
+        raise ShapeError(f"{heads} K / {len(v_dst)} V destinations (1..{_lib.DF_MAX_HEADS} heads per launch)")
+    _bf16_rows(x, "x")
+    hw, in_dim = x.shape
+    _bf16_rows(w_qkv, "w_qkv", in_dim)
+    if w_qkv.shape[0] != 3 * heads * head_dim:
+        raise ShapeError(f"w_qkv has {w_qkv.shape[0]} rows, expected 3*{heads}*{head_dim}")
+    if q_out.dtype != torch.bfloat16 or tuple(q_out.shape) != (heads, hw, head_dim) or not q_out.is_contiguous():
+        raise ShapeError(f"q_out must be contiguous bf16 {(heads, hw, head_dim)}, got {tuple(q_out.shape)}")
+    ld = None
+    for t in list(k_dst) + list(v_dst):
+        if t.dtype != torch.bfloat16 or tuple(t.shape) != (hw, head_dim) or t.stride(1) != 1:
+            raise ShapeError(f"K/V destination must be a bf16 ({hw}, {head_dim}) row view, got {tuple(t.shape)}")
+        ld = t.stride(0) if ld is None else ld
+        if t.stride(0) != ld:
+            raise ShapeError("K/V destinations must share one row stride")
+    args = _lib.QkvArgs()
+    args.x, args.w_qkv = x.data_ptr(), w_qkv.data_ptr()
+    args.hw, args.num_heads, args.head_dim, args.in_dim = hw, heads, head_dim, in_dim
+    args.q_out = q_out.data_ptr()
+    for h in range(heads):
+        args.k_dst[h] = k_dst[h].data_ptr()
+        args.v_dst[h] = v_dst[h].data_ptr()
+    args.kv_ld = ld
+    return PreparedLaunch("df_qkv_project", (ctypes.byref(args),), (args, x, w_qkv, q_out, k_dst, v_dst))
+
+
+def prepare_out_projection(o: torch.Tensor, w_o: torch.Tensor, x: torch.Tensor, x_bf16: torch.Tensor | None,
+                           head_dim: int) -> PreparedLaunch:
+    """df_out_project: ``x += merge(o) @ W_o`` (scenario.py:116-120 + engine.py:443 residual).
+
+    ``o`` bf16 [heads, hw, head_dim] contiguous (the FMHA output); ``w_o`` bf16
+    [out_dim, heads*head_dim]; ``x`` fp32 [hw, out_dim] updated in place;
+    ``x_bf16`` (optional) bf16 [hw, out_dim] receives the updated x.
+    """
+    if o.dtype != torch.bfloat16 or o.dim() != 3 or o.shape[2] != head_dim or not o.is_contiguous():
+        raise ShapeError(f"o must be contiguous bf16 (heads, hw, {head_dim}), got {tuple(o.shape)}")
+    heads, hw, _ = o.shape
+    _bf16_rows(w_o, "w_o", heads * head_dim)
+    out_dim = w_o.shape[0]
+    if x.dtype != torch.float32 or tuple(x.shape) != (hw, out_dim) or not x.is_contiguous():
+        raise ShapeError(f"x must be contiguous fp32 ({hw}, {out_dim}), got {x.dtype} {tuple(x.shape)}")
+    if x_bf16 is not None and (x_bf16.dtype != torch.bfloat16 or tuple(x_bf16.shape) != (hw, out_dim)
+                               or not x_bf16.is_contiguous()):
+        raise ShapeError(f"x_bf16 must be contiguous bf16 ({hw}, {out_dim})")
+    args = _lib.OprojArgs()
+    args.o, args.w_o = o.data_ptr(), w_o.data_ptr()
+    args.hw, args.num_heads, args.head_dim, args.out_dim = hw, heads, head_dim, out_dim
+    args.x = x.data_ptr()
+    args.x_bf16 = x_bf16.data_ptr() if x_bf16 is not None else None
+    return PreparedLaunch("df_out_project", (ctypes.byref(args),), (args, o, w_o, x, x_bf16))

@@ -178,6 +178,8 @@ def _block_segments(block: FrameBlock, st: RingStorage, slot: int, device) -> li
         if d % 8 or t.stride(1) != 1 or (t.stride(0) * 2) % 16 or t.data_ptr() % 16:
             t = torch.nn.functional.pad(t, (0, (-d) % 8)).contiguous()
         dst = plane[st.rows(slot)]
+        if t.data_ptr() == dst.data_ptr() and t.stride(0) == dst.stride(0):
+            continue  # produced in place (df_qkv_project wrote the pending slot): nothing to move
         segs.append((t.data_ptr(), dst.data_ptr(), st.hw, t.stride(0) * 2, width * 2, _row_bytes(d)))
         # keep the temporary alive until the copy is enqueued
         segs[-1] = segs[-1] + (t,)
@@ -240,6 +242,17 @@ class HeadKVCache:
             r = st.rows(self.slot_of(f))
             out.append(FrameBlock(f, st.arena.k[r, : st.head_dim], st.arena.v[r, : st.head_dim]))
         return out
+
+    def pending_view(self, hw: int, head_dim: int, device=None) -> tuple[torch.Tensor, torch.Tensor]:
+        """(K, V) bf16 [hw, head_dim] views of the pending slot.
+
+        A producer (``df_qkv_project``) may write the current frame here in
+        place; a FrameBlock over these views then stages and appends with no
+        copy at all.
+        """
+        st = self.ensure_storage(hw, head_dim, device)
+        r = st.rows(self.pending_slot)
+        return st.arena.k[r, :head_dim], st.arena.v[r, :head_dim]
 
     def past_tokens(self) -> int:
         return len(self) * (self.storage.hw if self.storage else 0)
