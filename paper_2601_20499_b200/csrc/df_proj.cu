@@ -11,13 +11,15 @@
 //                   straight from the FMHA output, so the head merge
 //                   (transpose) costs nothing.
 //
-// Persistent kernel, one CTA per SM, 192 threads:
+// Persistent kernel, one CTA per SM, 320 threads:
 //   warp 0      TMA producer: [128 x 64] A box + [BN x 64] B box per stage
 //               (SWIZZLE_128B), kStages-deep ring
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer,
 //               accumulators double-buffered in TMEM (2 x BN fp32 columns)
-//   warps 2-5   epilogue: tcgen05.ld 32 columns at a time, fused stores,
-//               overlapping the next tile's main loop
+//   warps 2-9   epilogue (two per TMEM lane quadrant, half the columns
+//               each): tcgen05.ld 32 columns, staged through shared memory,
+//               row-contiguous fused loads/stores, overlapping the next
+//               tile's main loop
 // Tiles are walked m-fastest so consecutive CTAs share the same W tile in L2.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -36,19 +38,34 @@ namespace {
 
 constexpr int kPBM = 128;
 constexpr int kPBK = 64;  // one 128-byte swizzle atom of bf16 per stage
-constexpr int kPThreads = 192;
+constexpr int kEpiWarps = 8;  // two per TMEM lane quadrant, each half of the tile's columns
+constexpr int kPThreads = 64 + 32 * kEpiWarps;
 
 enum { kEpiQKV = 0, kEpiOut = 1 };
 
-template <int BN>
+// Per epilogue warp, one 32-column chunk of its 32 rows is staged in shared
+// memory (rows padded by 16 B: conflict-free row-per-lane writes), then
+// written out row-contiguously (4-8 rows x 64-128 B per warp instruction).
+template <int kEpi>
+struct StageRow {
+  static constexpr int kBytes = kEpi == kEpiQKV ? 64 + 16 : 128 + 16;  // bf16 / fp32 chunk row
+};
+
+template <int BN, int kEpi>
 struct ProjCfg {
-  static constexpr int kStages = BN == 256 ? 4 : 6;
   static constexpr int kABytes = kPBM * kPBK * 2;
   static constexpr int kBBytes = BN * kPBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kBarOff = kStages * kStageBytes;
+  static constexpr int kStgWarp = 32 * StageRow<kEpi>::kBytes;
+  static constexpr int kBudget = 232448 - 1024 - 256;
+  static constexpr int kFit = (kBudget - kEpiWarps * kStgWarp) / kStageBytes;
+  static constexpr int kStages = kFit > 6 ? 6 : kFit;
+  static constexpr int kStgOff = kStages * kStageBytes;
+  static constexpr int kBarOff = kStgOff + kEpiWarps * kStgWarp;
   static constexpr int kSmem = kBarOff + (2 * kStages + 4) * 8 + 16 + 1024;
-  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;  // power of two
+  static_assert(kStages >= 3, "pipeline too shallow");
+  static_assert(kSmem <= 232448, "shared memory");
 };
 
 struct ProjParams {
@@ -69,57 +86,93 @@ struct ProjParams {
   __nv_bfloat16* x_bf16;
 };
 
-__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* f) {
-  uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    uint4 v;
-    v.x = pack_bf16x2(f[8 * i + 0], f[8 * i + 1]);
-    v.y = pack_bf16x2(f[8 * i + 2], f[8 * i + 3]);
-    v.z = pack_bf16x2(f[8 * i + 4], f[8 * i + 5]);
-    v.w = pack_bf16x2(f[8 * i + 6], f[8 * i + 7]);
-    d4[i] = v;
-  }
-}
-
+// One 32-column chunk (accumulator registers r, thread = row `lane` of the
+// warp's 32 rows starting at tile row `row0`).
 template <int kEpi>
-__device__ __forceinline__ void epilogue_chunk(const ProjParams& p, int row, int n0, const uint32_t* r) {
-  float f[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(r[i]);
+__device__ __forceinline__ void epilogue_chunk(const ProjParams& p, uint8_t* stg, int lane, int row0, int n0,
+                                               const uint32_t (&r)[32]) {
+  constexpr int kRow = StageRow<kEpi>::kBytes;
   if constexpr (kEpi == kEpiQKV) {
-    const int which = n0 / p.qkv_cols;  // 0 q, 1 k, 2 v
-    const int rem = n0 - which * p.qkv_cols;
-    const int h = rem / p.head_dim;
-    const int col = rem - h * p.head_dim;
-    __nv_bfloat16* dst;
-    if (which == 0)
-      dst = p.q_out + (static_cast<int64_t>(h) * p.hw + row) * p.head_dim + col;
-    else
-      dst = (which == 1 ? p.k_dst[h] : p.v_dst[h]) + static_cast<int64_t>(row) * p.kv_ld + col;
-    store_bf16x32(dst, f);
-  } else {
-    float4* x4 = reinterpret_cast<float4*>(p.x + static_cast<int64_t>(row) * p.out_ld + n0);
+    uint4* srow = reinterpret_cast<uint4*>(stg + lane * kRow);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float4 a = x4[i];
-      a.x += f[4 * i + 0];
-      a.y += f[4 * i + 1];
-      a.z += f[4 * i + 2];
-      a.w += f[4 * i + 3];
-      x4[i] = a;
-      f[4 * i + 0] = a.x;
-      f[4 * i + 1] = a.y;
-      f[4 * i + 2] = a.z;
-      f[4 * i + 3] = a.w;
+    for (int i = 0; i < 4; ++i) {
+      uint4 v;
+      v.x = pack_bf16x2(__uint_as_float(r[8 * i + 0]), __uint_as_float(r[8 * i + 1]));
+      v.y = pack_bf16x2(__uint_as_float(r[8 * i + 2]), __uint_as_float(r[8 * i + 3]));
+      v.z = pack_bf16x2(__uint_as_float(r[8 * i + 4]), __uint_as_float(r[8 * i + 5]));
+      v.w = pack_bf16x2(__uint_as_float(r[8 * i + 6]), __uint_as_float(r[8 * i + 7]));
+      srow[i] = v;
     }
-    if (p.x_bf16) store_bf16x32(p.x_bf16 + static_cast<int64_t>(row) * p.out_ld + n0, f);
+    __syncwarp();
+    if (n0 < p.n) {
+      const int which = n0 / p.qkv_cols;  // 0 q, 1 k, 2 v (warp-uniform)
+      const int rem = n0 - which * p.qkv_cols;
+      const int h = rem / p.head_dim;
+      const int col = rem - h * p.head_dim;
+      __nv_bfloat16* base;
+      int64_t ld;
+      if (which == 0) {
+        base = p.q_out + static_cast<int64_t>(h) * p.hw * p.head_dim + col;
+        ld = p.head_dim;
+      } else {
+        base = (which == 1 ? p.k_dst[h] : p.v_dst[h]) + col;
+        ld = p.kv_ld;
+      }
+      const int piece = lane & 3;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int rl = 8 * k + (lane >> 2);
+        const int row = row0 + rl;
+        if (row < p.m)
+          *reinterpret_cast<uint4*>(base + row * ld + piece * 8) =
+              *reinterpret_cast<const uint4*>(stg + rl * kRow + piece * 16);
+      }
+    }
+    __syncwarp();
+  } else {
+    float4* srow = reinterpret_cast<float4*>(stg + lane * kRow);
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      srow[i] = make_float4(__uint_as_float(r[4 * i + 0]), __uint_as_float(r[4 * i + 1]),
+                            __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+    __syncwarp();
+    if (n0 < p.n) {
+      const int piece = lane & 7;
+      float4 xv[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int row = row0 + 4 * k + (lane >> 3);
+        if (row < p.m) xv[k] = *reinterpret_cast<const float4*>(p.x + static_cast<int64_t>(row) * p.out_ld + n0 + 4 * piece);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int rl = 4 * k + (lane >> 3);
+        const int row = row0 + rl;
+        if (row < p.m) {
+          const float4 a = *reinterpret_cast<const float4*>(stg + rl * kRow + piece * 16);
+          float4 v = xv[k];
+          v.x += a.x;
+          v.y += a.y;
+          v.z += a.z;
+          v.w += a.w;
+          const int64_t off = static_cast<int64_t>(row) * p.out_ld + n0 + 4 * piece;
+          *reinterpret_cast<float4*>(p.x + off) = v;
+          if (p.x_bf16) {
+            uint2 b;
+            b.x = pack_bf16x2(v.x, v.y);
+            b.y = pack_bf16x2(v.z, v.w);
+            *reinterpret_cast<uint2*>(p.x_bf16 + off) = b;
+          }
+        }
+      }
+    }
+    __syncwarp();
   }
 }
 
 template <int BN, int kEpi>
 __global__ void __launch_bounds__(kPThreads, 1) df_proj_kernel(const __grid_constant__ ProjParams p) {
-  using C = ProjCfg<BN>;
+  using C = ProjCfg<BN, kEpi>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
@@ -138,7 +191,7 @@ __global__ void __launch_bounds__(kPThreads, 1) df_proj_kernel(const __grid_cons
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(acc_full + a, 1);
-      mbar_init(acc_empty + a, 4);  // one arrive per epilogue warp
+      mbar_init(acc_empty + a, kEpiWarps);  // one arrive per epilogue warp
     }
     fence_mbar_init();
   }
@@ -210,6 +263,9 @@ __global__ void __launch_bounds__(kPThreads, 1) df_proj_kernel(const __grid_cons
   } else {
     // ------------------------------------------------------------ epilogue
     const int quad = warp & 3;  // TMEM lanes 32*quad .. 32*quad+31
+    constexpr int kPer = BN / 64;  // 32-column chunks per epilogue warp
+    const int c0 = ((warp - 2) >> 2) * kPer;
+    uint8_t* stg = smem + C::kStgOff + (warp - 2) * C::kStgWarp;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
@@ -217,15 +273,18 @@ __global__ void __launch_bounds__(kPThreads, 1) df_proj_kernel(const __grid_cons
       const int nb = tile / p.m_tiles;
       mbar_wait(acc_full + acc, acc_phase);
       tc_fence_after();
-      const int row = mb * kPBM + quad * 32 + lane;
+      const int row0 = mb * kPBM + quad * 32;
       const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(quad * 32) << 16);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < kPer; ++c) {
         uint32_t r[32];
-        tmem_ld32(taddr + c * 32, r);
+        tmem_ld32(taddr + (c0 + c) * 32, r);
         tmem_wait_ld();
-        const int n0 = nb * BN + c * 32;
-        if (row < p.m && n0 < p.n) epilogue_chunk<kEpi>(p, row, n0, r);
+#ifndef DF_PROJ_DIAG
+        epilogue_chunk<kEpi>(p, stg, lane, row0, nb * BN + (c0 + c) * 32, r);
+#else
+        if (row0 < 0) epilogue_chunk<kEpi>(p, stg, lane, row0, nb * BN + (c0 + c) * 32, r);
+#endif
       }
       tc_fence_before();
       __syncwarp();
@@ -250,37 +309,47 @@ int launch_proj(const ProjParams& p, int grid, cudaStream_t stream) {
   auto kern = df_proj_kernel<BN, kEpi>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ProjCfg<BN>::kSmem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ProjCfg<BN, kEpi>::kSmem);
     if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(df_proj_kernel)", e);
     configured = true;
   }
-  kern<<<grid, kPThreads, ProjCfg<BN>::kSmem, stream>>>(p);
+  kern<<<grid, kPThreads, ProjCfg<BN, kEpi>::kSmem, stream>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("df_proj_kernel launch", e);
   return DF_OK;
 }
 
-// Tile width: fewest tensor-pipe "tile-columns" over whole waves of the
-// persistent grid (N=128 tiles pay ~6% more per FLOP than N=256 ones).
+// Tile width N: smallest modelled time over whole waves of the persistent
+// grid.  Per-tile cost ~ N / eff(N): with both operands in shared memory an
+// N=128 tile is bound by shared-memory bandwidth (measured 0.66 of the N=256
+// rate on B200), N=192 at 0.86.
 int pick_bn(int64_t m, int64_t n) {
   if (const char* env = std::getenv("DF_PROJ_BN")) {
     const int v = std::atoi(env);
-    if (v == 128 || v == 256) return v;
+    if (v == 128 || v == 192 || v == 256) return v;
   }
   const int64_t sms = sm_count_cached();
   const int64_t mt = (m + kPBM - 1) / kPBM;
   double best = 1e300;
-  int bn = 128;
-  for (int cand : {256, 128}) {
+  int bn = 256;
+  for (int cand : {256, 192, 128}) {
+    const double eff = cand == 256 ? 1.0 : (cand == 192 ? 0.86 : 0.66);
     const int64_t tiles = mt * ((n + cand - 1) / cand);
     const int64_t waves = (tiles + sms - 1) / sms;
-    const double cost = double(waves) * cand * (cand == 128 ? 1.06 : 1.0);
-    if (cost < best) {
+    const double cost = double(waves) * cand / eff;
+    if (cost < best * 0.999) {
       best = cost;
       bn = cand;
     }
   }
   return bn;
+}
+
+template <int kEpi>
+int launch_bn(int bn, const ProjParams& p, int grid, cudaStream_t s) {
+  if (bn == 256) return launch_proj<256, kEpi>(p, grid, s);
+  if (bn == 192) return launch_proj<192, kEpi>(p, grid, s);
+  return launch_proj<128, kEpi>(p, grid, s);
 }
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
@@ -334,7 +403,7 @@ extern "C" int df_qkv_project(const df_qkv_args* a, void* stream) {
   p.tiles = p.m_tiles * ((p.n + bn - 1) / bn);
   const int grid = p.tiles < sm_count_cached() ? p.tiles : sm_count_cached();
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  return bn == 256 ? launch_proj<256, kEpiQKV>(p, grid, s) : launch_proj<128, kEpiQKV>(p, grid, s);
+  return launch_bn<kEpiQKV>(bn, p, grid, s);
 }
 
 extern "C" int df_out_project(const df_oproj_args* a, void* stream) {
@@ -367,5 +436,5 @@ extern "C" int df_out_project(const df_oproj_args* a, void* stream) {
   p.tiles = p.m_tiles * ((p.n + bn - 1) / bn);
   const int grid = p.tiles < sm_count_cached() ? p.tiles : sm_count_cached();
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  return bn == 256 ? launch_proj<256, kEpiOut>(p, grid, s) : launch_proj<128, kEpiOut>(p, grid, s);
+  return launch_bn<kEpiOut>(bn, p, grid, s);
 }

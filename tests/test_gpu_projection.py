@@ -30,7 +30,7 @@ def _rel(got: torch.Tensor, want: torch.Tensor) -> float:
     return float((got - want).abs().max() / want.abs().max().clamp_min(1e-30))
 
 
-@pytest.fixture(params=[None, "128", "256"], ids=["auto", "bn128", "bn256"])
+@pytest.fixture(params=[None, "128", "192", "256"], ids=["auto", "bn128", "bn192", "bn256"])
 def tile_n(request, monkeypatch):
     if request.param is not None:
         monkeypatch.setenv("DF_PROJ_BN", request.param)
