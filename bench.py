@@ -215,6 +215,71 @@ def time_steps(fn, steps, warmup):
     return e0.elapsed_time(e1) / steps, all_lcs
 
 
+def full_layer(df, cfg, packed, classes, dev, gen, args, ws, bf16_peak):
+    """the whole attention block of a layer on the device.
+
+    x (fp32 residual + bf16 copy) -> df_qkv_project (Q + K/V written into the
+    pending ring slots) -> packed_step (ONE FMHA, no staging copy) ->
+    df_out_project (head merge @ W_o + residual).  Random W (x @ W scale
+    1/sqrt(D)); reported beside the attention-only metric, not in `value`.
+    """
+    import torch
+
+    from paper_2601_20499_b200 import kernels as K
+
+    Dm = H * D
+    wqkv = [(torch.randn(3 * Dm, Dm, device=dev, generator=gen) / Dm**0.5).to(torch.bfloat16) for _ in range(L)]
+    wo = [(torch.randn(Dm, Dm, device=dev, generator=gen) / Dm**0.5).to(torch.bfloat16) for _ in range(L)]
+    xs = df.ResidualStream(torch.randn(HW, Dm, device=dev, generator=gen))
+    views = [[c.pending_view(HW, D, dev) for c in packed[layer]] for layer in range(L)]
+    qbuf = [torch.empty(H, HW, D, dtype=torch.bfloat16, device=dev) for _ in range(L)]
+    proj = [K.prepare_qkv_projection(xs.bf16, wqkv[layer], qbuf[layer], [kv[0] for kv in views[layer]],
+                                     [kv[1] for kv in views[layer]], D) for layer in range(L)]
+    blocks = [[df.FrameBlock(W, k, v) for k, v in views[layer]] for layer in range(L)]
+    split = {"qkv": 0.0, "attn": 0.0, "oproj": 0.0}
+
+    def step(ev=None):
+        for layer in range(L):
+            if ev is not None:
+                ev[layer][0].record()
+            proj[layer].launch()
+            if ev is not None:
+                ev[layer][1].record()
+            out, _ = df.packed_step(qbuf[layer], packed[layer], blocks[layer], classes, cfg)
+            if ev is not None:
+                ev[layer][2].record()
+            K.prepare_out_projection(out, wo[layer], xs.f32, xs.bf16, D).launch()
+            if ev is not None:
+                ev[layer][3].record()
+        return []
+
+    barrier(ws)
+    t, _ = time_steps(step, args.steps, args.warmup)
+    t = barrier_max(t, ws)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(L)]
+    step(ev)
+    torch.cuda.synchronize()
+    for e in ev:
+        split["qkv"] += e[0].elapsed_time(e[1]) / L
+        split["attn"] += e[1].elapsed_time(e[2]) / L
+        split["oproj"] += e[2].elapsed_time(e[3]) / L
+    fq, fo = 2 * HW * 3 * Dm * Dm, 2 * HW * Dm * Dm
+    tq, to = split["qkv"] * 1e-3, split["oproj"] * 1e-3
+    return {
+        "ms_per_step": t, "us_per_layer": t * 1e3 / L,
+        "fps": ws * FRAMES_PER_STEP / (DENOISE * t * 1e-3),
+        "split_us_per_layer": {k: v * 1e3 for k, v in split.items()},
+        "qkv_project": {"kernel": "df_proj_kernel<N,qkv>", "flops": fq, "tflops": fq / tq / 1e12,
+                        "frac": fq / tq / 1e12 / bf16_peak,
+                        "epilogue": "Q -> FMHA layout, K/V -> pending ring slots (no staging/append copy)"},
+        "out_project": {"kernel": "df_proj_kernel<N,out>", "flops": fo, "tflops": fo / to / 1e12,
+                        "frac": fo / to / 1e12 / bf16_peak,
+                        "epilogue": "x += merge(o) @ W_o (fp32 residual + bf16 copy)"},
+        "gpu_launches_per_layer": 3,
+        "path": "x -> df_qkv_project -> packed_step (1 FMHA) -> df_out_project, 30 layers per step",
+    }
+
+
 # ------------------------------------------------------------------ CPU leg
 def cpu_sample(reps: int = 1):
     """Oracle port (engine.py:87-137, fp64 numpy) on 1 neighbor + 1 sink + 1 dummy head of one warm layer."""
@@ -323,6 +388,8 @@ def gpu_arm(args, ws, rank, local):
     layer_ns = [lc.wall_time_ns for step in lcs for lc in step]
     launches = sum(lc.physical_launches for step in lcs for lc in step)
 
+    fused = full_layer(df, cfg, packed, classes, dev, gen, args, ws, bf16_peak)
+
     # e2e through the public API with host buffers
     pinned = [tuple(x.cpu().pin_memory() for x in layer) for layer in inputs]
     outs_host = [torch.empty(H, HW, D, dtype=torch.bfloat16).pin_memory() for _ in range(L)]
@@ -403,6 +470,7 @@ def gpu_arm(args, ws, rank, local):
                 "ms_per_step": t_e2e,
                 "path": "public packed_step per layer; pinned host Q/K/V H2D on a copy stream (double-buffered), "
                         "outputs D2H on a second stream, all inside the timed region"},
+        "layer_fused": fused,
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
