@@ -46,10 +46,14 @@ constexpr int kBN = 128;        // keys per kv tile
 constexpr int kWarps = 12;  // see role map above
 constexpr int kThreads = kWarps * 32;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
-#ifndef DF_EMU_EVERY
-#define DF_EMU_EVERY 8
+#ifndef DF_EMU_NUM
+#define DF_EMU_NUM 1
 #endif
-constexpr int kEmuEvery = DF_EMU_EVERY;  // 1 in kEmuEvery exp2 pairs runs as a polynomial on the FMA pipe
+// kEmuNum of every 8 exp2 pairs run as a polynomial on the FMA pipe (spread
+// evenly): MUFU ex2 is 16/clk/SM, so at d=128 exponentials alone need 100% of
+// the tensor-pipe time of a 2 x 128-row tile pair without this offload.
+constexpr int kEmuNum = DF_EMU_NUM;
+__host__ __device__ constexpr bool emulated_pair(int i) { return (i * kEmuNum) % 8 < kEmuNum; }
 
 struct HeadParam {
   int32_t base_row;
@@ -79,6 +83,7 @@ struct __align__(64) AttnParams {
   int32_t n_qpairs;
   int32_t max_slots;
   float scale_log2;
+  uint32_t exp_unit;  // 1 << 23 (exponent step of an fp32), see exp2_poly2
   int32_t item_prefix[DF_MAX_HEADS + 1];  // CTAs before head rank r (LPT order)
   uint8_t head_order[DF_MAX_HEADS];
   HeadParam heads[DF_MAX_HEADS];
@@ -302,16 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
         for (int c = 0; c < 128; ++c)
           if (c >= valid) r[c] = __float_as_uint(-INFINITY);
       }
-      float mx0 = __uint_as_float(r[0]), mx1 = __uint_as_float(r[1]);
-      float mx2 = __uint_as_float(r[2]), mx3 = __uint_as_float(r[3]);
-#pragma unroll
-      for (int c = 4; c < 128; c += 4) {
-        mx0 = fmaxf(mx0, __uint_as_float(r[c + 0]));
-        mx1 = fmaxf(mx1, __uint_as_float(r[c + 1]));
-        mx2 = fmaxf(mx2, __uint_as_float(r[c + 2]));
-        mx3 = fmaxf(mx3, __uint_as_float(r[c + 3]));
-      }
-      const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+      const float m_tile = row_max128(r) * sl2;
       if (jj == 0) {
         m = m_tile;
       } else {
@@ -360,8 +356,8 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
           const int c = quarter * 32 + 2 * i;
           const float2 x = fma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
           float2 e;
-          if ((c / 2) % kEmuEvery == kEmuEvery - 1) {  // compile-time: every kEmuEvery-th pair on the FMA pipe
-            e = exp2_poly2(x);
+          if (emulated_pair(c / 2)) {  // compile-time: kEmuNum of every 8 pairs on the FMA pipe
+            e = exp2_poly2(x, p.exp_unit);
           } else {
             e = make_float2(ex2(x.x), ex2(x.y));
           }
@@ -735,16 +731,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int c = 0; c < 128; ++c)
           if (c >= valid) r[c] = __float_as_uint(-INFINITY);
       }
-      float mx0 = __uint_as_float(r[0]), mx1 = __uint_as_float(r[1]);
-      float mx2 = __uint_as_float(r[2]), mx3 = __uint_as_float(r[3]);
-#pragma unroll
-      for (int c = 4; c < 128; c += 4) {
-        mx0 = fmaxf(mx0, __uint_as_float(r[c + 0]));
-        mx1 = fmaxf(mx1, __uint_as_float(r[c + 1]));
-        mx2 = fmaxf(mx2, __uint_as_float(r[c + 2]));
-        mx3 = fmaxf(mx3, __uint_as_float(r[c + 3]));
-      }
-      const float m_tile = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * sl2;
+      const float m_tile = row_max128(r) * sl2;
       if (jj == 0) {
         m = m_tile;
       } else {
@@ -793,8 +780,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int c = quarter * 32 + 2 * i;
           const float2 x = fma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
           float2 e;
-          if ((c / 2) % kEmuEvery == kEmuEvery - 1) {
-            e = exp2_poly2(x);
+          if (emulated_pair(c / 2)) {
+            e = exp2_poly2(x, p.exp_unit);
           } else {
             e = make_float2(ex2(x.x), ex2(x.y));
           }
@@ -1233,6 +1220,7 @@ extern "C" int df_attn_fwd(const df_attn_args* a, void* stream) {
   p.row_sampled = a->row_sampled;
   p.probe_rows = a->probe_rows;
   p.scale_log2 = a->scale * 1.4426950408889634f;
+  p.exp_unit = 1u << 23;
 
   int64_t groups = 0, slots = 0;
   for (int i = 0; i < a->num_heads; ++i) {

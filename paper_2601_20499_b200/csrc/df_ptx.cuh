@@ -289,7 +289,7 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) {
 // rounding of P), 2^j added into the exponent field.  x is clamped at -126 (a
 // result < 1 has exponent 126, so j >= -126 keeps the sum >= 0): masked (-inf)
 // columns give ~1e-38 instead of exactly 0 (tests/test_gpu_attn_kernel.py).
-__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+__device__ __forceinline__ float2 exp2_poly2(float2 x, uint32_t exp_unit) {
   x.x = fmaxf(x.x, -126.f);
   x.y = fmaxf(x.y, -126.f);
   const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
@@ -299,9 +299,30 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   float2 q = fma2(f, make_float2(0.05517132f, 0.05517132f), make_float2(0.24261054f, 0.24261054f));
   q = fma2(q, f, make_float2(0.69326099f, 0.69326099f));
   q = fma2(q, f, make_float2(0.99992811f, 0.99992811f));
-  q.x = __int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23));
-  q.y = __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23));
-  return q;
+  // q += j << 23 as IMAD (exp_unit = 2^23 is a launch parameter, so ptxas cannot
+  // turn it into a shift): integer multiply-add issues on the FMA pipe and keeps
+  // the ALU pipe (row max, clamps) free.
+  uint32_t qx = __float_as_uint(q.x), qy = __float_as_uint(q.y);
+  asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(qx) : "r"(__float_as_uint(t.x)), "r"(exp_unit));
+  asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(qy) : "r"(__float_as_uint(t.y)), "r"(exp_unit));
+  return make_float2(__uint_as_float(qx), __uint_as_float(qy));
+}
+
+// 3-input max (FMNMX3 on sm_100a): a 128-wide row max in 64 ALU issues instead of 127.
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float row_max128(const uint32_t* r) {
+  float mx[4] = {__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]), __uint_as_float(r[3])};
+#pragma unroll
+  for (int c = 4; c < 124; c += 8)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) mx[k] = fmax3(mx[k], __uint_as_float(r[c + 2 * k]), __uint_as_float(r[c + 2 * k + 1]));
+  mx[0] = fmax3(mx[0], __uint_as_float(r[124]), __uint_as_float(r[125]));
+  mx[1] = fmax3(mx[1], __uint_as_float(r[126]), __uint_as_float(r[127]));
+  return fmax3(mx[0], mx[1], fmaxf(mx[2], mx[3]));
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
