@@ -89,6 +89,21 @@ struct __align__(64) AttnParams {
   HeadParam heads[DF_MAX_HEADS];
 };
 
+#ifdef DF_TRACE
+// Dev-only timeline of CTA 0 (clock64 stamps): softmax warps 4 / 8 (lane 0)
+// and the MMA issuer, first kTraceIters kv tiles.  Read with df_trace_fetch.
+constexpr int kTraceIters = 128;
+__device__ unsigned long long g_trace[3][kTraceIters][10];
+#define DF_STAMP(who, it, k)                                                        \
+  do {                                                                              \
+    if (blockIdx.x == 0 && (it) < kTraceIters) g_trace[who][it][k] = clock64();      \
+  } while (0)
+#else
+#define DF_STAMP(who, it, k) \
+  do {                       \
+  } while (0)
+#endif
+
 template <int D>
 struct AttnCfg {
 #ifndef DF_STAGES_K128
@@ -218,66 +233,78 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc_qk = idesc_bf16(kBM, kBN, false);
-      constexpr uint32_t idesc_pv = idesc_bf16(kBM, D, true);
-      const uint32_t sQ = smem_u32(smem + C::kQOff);
-      const uint32_t sK = smem_u32(smem + C::kKOff);
-      const uint32_t sV = smem_u32(smem + C::kVOff);
-      const uint32_t tS0 = tmem, tS1 = tmem + 128;
-      const uint32_t tO0 = tmem + C::kTmemO, tO1 = tmem + C::kTmemO + D;
+    // The whole warp walks the loop (operands warp-uniform), one elected lane
+    // issues; descriptors are precomputed 64-bit bases plus compile-time
+    // offsets, so a UMMA costs ~1-2 issue slots on a sub-partition shared with
+    // two softmax warps.
+    constexpr uint32_t idesc_qk = idesc_bf16(kBM, kBN, false);
+    constexpr uint32_t idesc_pv = idesc_bf16(kBM, D, true);
+    const uint64_t dQ = sdesc_sw128(smem_u32(smem + C::kQOff), 16, 1024);
+    const uint64_t dK = sdesc_sw128(smem_u32(smem + C::kKOff), 16, 1024);
+    const uint64_t dV = sdesc_sw128(smem_u32(smem + C::kVOff), C::kBoxBytes, 1024);
+    constexpr uint64_t kTileDesc = C::kTileBytes >> 4;  // descriptor units (16 B)
+    const uint32_t tS0 = tmem, tS1 = tmem + 128;
+    const uint32_t tO0 = tmem + C::kTmemO, tO1 = tmem + C::kTmemO + D;
 
-      auto qk = [&](uint32_t d_tmem, int t, int ks) {
-        const uint32_t qa = sQ + t * C::kTileBytes;
-        const uint32_t kb = sK + ks * C::kTileBytes;
+    auto qk = [&](uint32_t d_tmem, int t, int ks) {
+      const uint64_t qa = dQ + t * kTileDesc;
+      const uint64_t kb = dK + ks * kTileDesc;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * C::kBoxBytes + (kk & 3) * 32;
-          umma_ss(d_tmem, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(kb + off, 16, 1024), idesc_qk, kk > 0);
-        }
-      };
-      auto pv = [&](int t, int jj) {
-        const int vs = jj % C::kStagesV;
-        mbar_wait(p_full + 2 * t, jj & 1);  // first half of P (keys 0-63) is in TMEM
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint64_t off = ((kk >> 2) * C::kBoxBytes + (kk & 3) * 32) >> 4;
+#ifndef DF_DIAG_NO_MMA
+        umma_ss_elect(d_tmem, qa + off, kb + off, idesc_qk, kk > 0);
+#endif
+      }
+    };
+    auto pv = [&](int t, int jj) {
+      const int vs = jj % C::kStagesV;
+      mbar_wait(p_full + 2 * t, jj & 1);  // first half of P (keys 0-63) is in TMEM
+      tc_fence_after();
+      if (t == 0) {
+        mbar_wait(v_full + vs, (jj / C::kStagesV) & 1);
         tc_fence_after();
-        if (t == 0) {
-          mbar_wait(v_full + vs, (jj / C::kStagesV) & 1);
+      }
+      const uint64_t vb = dV + vs * kTileDesc;
+      const uint32_t tP = t ? tS1 : tS0;
+      const uint32_t tO = t ? tO1 : tO0;
+#pragma unroll
+      for (int kk = 0; kk < kBN / 16; ++kk) {
+        if (kk == kBN / 32) {  // second half of P (keys 64-127)
+          mbar_wait(p_full + 2 * t + 1, jj & 1);
           tc_fence_after();
         }
-        const uint32_t vb = sV + vs * C::kTileBytes;
-        const uint32_t tP = t ? tS1 : tS0;
-        const uint32_t tO = t ? tO1 : tO0;
-#pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk) {
-          if (kk == kBN / 32) {  // second half of P (keys 64-127)
-            mbar_wait(p_full + 2 * t + 1, jj & 1);
-            tc_fence_after();
-          }
-          umma_ts(tO, tP + kk * 8, sdesc_sw128(vb + kk * 2048, C::kBoxBytes, 1024), idesc_pv,
-                  (jj > 0 || kk > 0) ? 1u : 0u);
-        }
-        umma_commit(o_full + t);
-        if (t == 1 || !two) umma_commit(v_empty + vs);  // last reader of V_jj
-      };
-
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      for (int jj = 0; jj < n_kv; ++jj) {
-        const int ks = jj % C::kStagesK;
-        mbar_wait(k_full + ks, (jj / C::kStagesK) & 1);
-        tc_fence_after();
-        qk(tS0, 0, ks);
-        umma_commit(s_full + 0);
-        if (two) {
-          if (jj > 0) pv(1, jj - 1);
-          qk(tS1, 1, ks);
-          umma_commit(s_full + 1);
-        }
-        umma_commit(k_empty + ks);
-        pv(0, jj);
+#ifndef DF_DIAG_NO_MMA
+        umma_ts_elect(tO, tP + kk * 8, vb + ((kk * 2048) >> 4), idesc_pv, (jj > 0 || kk > 0) ? 1u : 0u);
+#endif
       }
-      if (two) pv(1, n_kv - 1);
+      umma_commit_elect(o_full + t);
+      if (t == 1 || !two) umma_commit_elect(v_empty + vs);  // last reader of V_jj
+    };
+
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    for (int jj = 0; jj < n_kv; ++jj) {
+      const int ks = jj % C::kStagesK;
+      if (lane == 0) DF_STAMP(2, jj, 0);
+      mbar_wait(k_full + ks, (jj / C::kStagesK) & 1);
+      tc_fence_after();
+      if (lane == 0) DF_STAMP(2, jj, 1);
+      qk(tS0, 0, ks);
+      umma_commit_elect(s_full + 0);
+      if (two) {
+        if (lane == 0) DF_STAMP(2, jj, 2);
+        if (jj > 0) pv(1, jj - 1);
+        if (lane == 0) DF_STAMP(2, jj, 3);
+        qk(tS1, 1, ks);
+        umma_commit_elect(s_full + 1);
+      }
+      umma_commit_elect(k_empty + ks);
+      if (lane == 0) DF_STAMP(2, jj, 4);
+      pv(0, jj);
+      if (lane == 0) DF_STAMP(2, jj, 5);
     }
+    if (two) pv(1, n_kv - 1);
   } else if (warp >= 4 && (two || warp < 8)) {
     // ------------------------------------------------------------ softmax
     const int t = (warp - 4) >> 2;        // query tile of this warpgroup
@@ -291,16 +318,20 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
     float l = 0.f;
     float reg_acc[3] = {0.f, 0.f, 0.f};  // probe: sink / neighbor / current mass
 
+    const bool stamp = lane == 0 && quad == 0;
     for (int jj = 0; jj < n_kv; ++jj) {
       const int j = kv_begin + jj;
+      if (stamp) DF_STAMP(t, jj, 0);
       mbar_wait(s_full + t, jj & 1);
       tc_fence_after();
+      if (stamp) DF_STAMP(t, jj, 1);
       uint32_t r[128];
       tmem_ld32(tS + 0, r + 0);
       tmem_ld32(tS + 32, r + 32);
       tmem_ld32(tS + 64, r + 64);
       tmem_ld32(tS + 96, r + 96);
       tmem_wait_ld();
+      if (stamp) DF_STAMP(t, jj, 2);
       const int valid = hd.n_tok - j * kBN;
       if (valid < kBN) {
 #pragma unroll
@@ -308,6 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
           if (c >= valid) r[c] = __float_as_uint(-INFINITY);
       }
       const float m_tile = row_max128(r) * sl2;
+      if (stamp) DF_STAMP(t, jj, 3);
       if (jj == 0) {
         m = m_tile;
       } else {
@@ -389,6 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(p_full + 2 * t);
+          if (stamp) DF_STAMP(t, jj, 4);
         }
       }
       if constexpr (kProbe) {
@@ -408,6 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(p_full + 2 * t + 1);
+      if (stamp) DF_STAMP(t, jj, 5);
     }
 
     // ------------------------------------------------------------ epilogue
@@ -1262,3 +1296,10 @@ extern "C" int df_attn_fwd(const df_attn_args* a, void* stream) {
     return probe ? launch_attn<128, true>(p, grid, s) : launch_attn<128, false>(p, grid, s);
   return probe ? launch_attn<64, true>(p, grid, s) : launch_attn<64, false>(p, grid, s);
 }
+
+#ifdef DF_TRACE
+extern "C" DF_API int df_trace_fetch(void* host, int64_t bytes) {
+  if (bytes > int64_t(sizeof(dfb::g_trace))) bytes = sizeof(dfb::g_trace);
+  return cudaMemcpyFromSymbol(host, dfb::g_trace, bytes) == cudaSuccess ? DF_OK : DF_E_CUDA;
+}
+#endif

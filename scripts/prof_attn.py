@@ -5,7 +5,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2601_20499_b200 import kernels as K
 dev = torch.device('cuda:0'); D = 128; HW = 4680
 mode = sys.argv[1] if len(sys.argv) > 1 else 'packed'
-ctxs = [28080] * 3 + [9360] * 9 if mode == 'packed' else [32760] * 12
+if mode == 'hires':
+    HW = 18720
+ctxs = {'packed': [28080] * 3 + [9360] * 9, 'baseline': [32760] * 12, 'hires': [131040] * 4}[mode]
 arena = K.KVArena(sum(K.KVArena.region_rows(c) for c in ctxs), D, dev)
 arena.k.normal_(); arena.v.normal_()
 q = torch.randn(len(ctxs) * HW, D, device=dev).to(torch.bfloat16)
