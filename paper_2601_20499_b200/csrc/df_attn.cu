@@ -325,6 +325,12 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
       mbar_wait(s_full + t, jj & 1);
       tc_fence_after();
       if (stamp) DF_STAMP(t, jj, 1);
+#ifdef DF_DIAG_NO_SOFTMAX  // dev: tensor-pipe-only timing (P = whatever S left in TMEM)
+      tc_fence_before();
+      mbar_arrive(p_full + 2 * t);
+      mbar_arrive(p_full + 2 * t + 1);
+      continue;
+#endif
       uint32_t r[128];
       tmem_ld32(tS + 0, r + 0);
       tmem_ld32(tS + 32, r + 32);
