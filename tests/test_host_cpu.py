@@ -196,3 +196,41 @@ def test_container_byte_compatible_with_reference(tmp_path):
         bad = tmp_path / "bad.dfc"
         bad.write_bytes(b"\x01")
         C.load_tensors(str(bad))
+
+
+def test_sweep_axis_rules_follow_reference_cli():
+    """cli.py:128-145 / 260-298 restated in paper_2601_20499_b200.sweep (no GPU needed)."""
+    from paper_2601_20499_b200 import sweep as S
+
+    sec = dict(num_layers=2, num_heads=4, head_dim=8, HW=6, window_len=3, ar_steps=6, denoise_steps=2,
+               dummy_count=4, probe_ar_step=2)
+    base = S.session_config(sec)
+    pts = S.axis_configs(base, "context_len", [4, 5])
+    assert [v for v, _ in pts] == [4.0, 5.0]
+    assert [(c.window_len, c.ar_steps) for _, c in pts] == [(3, 3), (4, 4)]
+    base4 = S.session_config({**sec, "window_len": 4, "ar_steps": 4})
+    pts = S.axis_configs(base4, "dummy_ratio", [0.0, 0.5, 1.0])
+    assert [c.dummy_count for _, c in pts] == [0, 4, 8] and all(c.ar_steps == 4 for _, c in pts)
+    assert S.axis_configs(base, "context_len", [4], HW=10)[0][1].HW == 10
+    frac = S.session_config({k: v for k, v in sec.items() if k != "dummy_count"} | {"dummy_fraction": 0.5})
+    assert frac.dummy_count == 4 and frac.packing_enabled
+    for bad in (lambda: S.axis_configs(base, "context_len", [3]),           # window < probe room
+                lambda: S.axis_configs(base, "context_len", [2]),           # < 3 frames
+                lambda: S.axis_configs(S.session_config({**sec, "window_len": 2}), "dummy_ratio", [0.5]),
+                lambda: S.axis_configs(base4, "dummy_ratio", [1.5]),
+                lambda: S.axis_configs(base, "context_len", []),
+                lambda: S.axis_configs(base, "heads", [1]),
+                lambda: S.session_config({**sec, "dummy_fraction": 0.5}),   # both count and fraction
+                lambda: S.session_config({"num_layers": 1}),
+                lambda: S.session_config({**sec, "bogus": 1})):
+        with pytest.raises(df.ConfigError):
+            bad()
+
+
+def test_sweep_cli_config_errors(tmp_path):
+    from paper_2601_20499_b200 import sweep as S
+
+    assert S.main(["--config", str(tmp_path / "missing.json"), "--axis", "context_len", "--out", "x.csv"]) == 2
+    p = tmp_path / "c.json"
+    p.write_text(json.dumps({"schema_version": 2, "session": {}}))
+    assert S.main(["--config", str(p), "--axis", "context_len", "--out", str(tmp_path / "o.csv")]) == 1
