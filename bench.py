@@ -263,6 +263,21 @@ def full_layer(df, cfg, packed, classes, dev, gen, args, ws, bf16_peak):
         split["qkv"] += e[0].elapsed_time(e[1]) / L
         split["attn"] += e[1].elapsed_time(e[2]) / L
         split["oproj"] += e[2].elapsed_time(e[3]) / L
+    # end to end with host buffers: the layer-0 input x comes from pinned host memory each step
+    # (the only per-step input once projections run on the device) and the output x goes back
+    x_host = torch.randn(HW, Dm, generator=torch.Generator().manual_seed(5)).pin_memory()
+    y_host = torch.empty(HW, Dm).pin_memory()
+
+    def e2e_step():
+        xs.f32.copy_(x_host, non_blocking=True)
+        xs.bf16.copy_(xs.f32)
+        step()
+        y_host.copy_(xs.f32, non_blocking=True)
+        return []
+
+    barrier(ws)
+    t_e2e, _ = time_steps(e2e_step, args.steps, args.warmup)
+    t_e2e = barrier_max(t_e2e, ws)
     fq, fo = 2 * HW * 3 * Dm * Dm, 2 * HW * Dm * Dm
     tq, to = split["qkv"] * 1e-3, split["oproj"] * 1e-3
     return {
@@ -276,6 +291,10 @@ def full_layer(df, cfg, packed, classes, dev, gen, args, ws, bf16_peak):
                         "frac": fo / to / 1e12 / bf16_peak,
                         "epilogue": "x += merge(o) @ W_o (fp32 residual + bf16 copy)"},
         "gpu_launches_per_layer": 3,
+        "e2e": {"value": ws * FRAMES_PER_STEP / (DENOISE * t_e2e * 1e-3), "unit": "latent frames/s (full attention "
+                "block: QKV + attention + out-projection)", "ms_per_step": t_e2e,
+                "h2d_bytes_per_step": HW * Dm * 4, "d2h_bytes_per_step": HW * Dm * 4,
+                "path": "pinned host x -> device, 30 fused layers, x -> pinned host, inside the timed region"},
         "path": "x -> df_qkv_project -> packed_step (1 FMHA) -> df_out_project, 30 layers per step",
     }
 
