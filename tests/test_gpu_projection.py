@@ -150,3 +150,19 @@ def test_projected_model_fused_equals_unfused_protocol():
     assert all(torch.equal(x.to(torch.bfloat16), getattr(y, "f32", y).to(torch.bfloat16)) for x, y in zip(a, b))
     assert ra.to_dict()["assignment"] == rb.to_dict()["assignment"]
     assert rb.physical_launches_steady == [2, 2]
+
+
+def test_projected_model_head_range_slices_weights():
+    """Head-parallel ranks project only their heads (ProjectedModel._w_heads): bitwise equal to the
+    corresponding heads of the full projection."""
+    _, toy = _toy_c1()
+    m = df.ProjectedModel(toy.weights, toy.frame_input, 4, 64, 192)
+    x = m.frame_input(0, 0)
+    q_full, k_full, v_full = m.qkv(1, x, 0, 0)
+    heads = range(1, 3)
+    q = torch.empty(2, 192, 64, dtype=torch.bfloat16, device="cuda")
+    k = torch.empty_like(q)
+    v = torch.empty_like(q)
+    m.qkv_into(1, x, 0, 0, q, list(k), list(v), heads=heads)
+    torch.cuda.synchronize()
+    assert torch.equal(q, q_full[1:3]) and torch.equal(k, k_full[1:3]) and torch.equal(v, v_full[1:3])
