@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -73,7 +74,7 @@ struct __align__(64) AttnParams {
   const uint8_t* region_tab;
   const uint8_t* row_sampled;
   float* probe_rows;
-  float* ws_o;           // split partials: [slot][256][D] unnormalised O
+  float* ws_o;           // split partials, unnormalised O: [slot][D/4][256] float4 (CTA pair: [slot][256][D])
   float* ws_ml;          // [slot][256][2] (running max in log2 units, row sum)
   int32_t* ws_cnt;       // [group] arrival counters (zero between launches)
   int64_t out_ld;
@@ -187,9 +188,13 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
     }
     fence_mbar_init();
   }
+  if (threadIdx.x == 0) DF_STAMP(2, kTraceIters - 1, 6);
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) DF_STAMP(2, kTraceIters - 1, 7);
+  const bool stamp_end = (threadIdx.x & 31) == 0 && ((threadIdx.x >> 5) == 4 || (threadIdx.x >> 5) == 8);
+  (void)stamp_end;
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -451,6 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
     }
 
     // ------------------------------------------------------------ epilogue
+    if (stamp) DF_STAMP(t, kTraceIters - 1, 6);
     mbar_wait(o_full + t, (n_kv - 1) & 1);
     tc_fence_after();
     const int prow = t * kBM + row_local;           // row within the pair
@@ -492,7 +498,10 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
       // split-KV: publish this piece's (O, m, l); the last piece of the pair combines.
       const int group = hd.group_base + qp;
       const int64_t slot0 = static_cast<int64_t>(hd.part_base) + static_cast<int64_t>(qp) * ns;
-      float* my_o = p.ws_o + ((slot0 + piece) * 2 * kBM + prow) * D;
+      // partial O layout [slot][D/4 float4 columns][256 rows]: the 32 rows of a warp
+      // write (and the combine reads) 512 contiguous bytes per instruction
+      constexpr int kRowsWs = 2 * kBM;
+      float4* my_o = reinterpret_cast<float4*>(p.ws_o) + (slot0 + piece) * (D / 4) * kRowsWs + prow;
 #pragma unroll
       for (int c = 0; c < D / 32; ++c) {
         uint32_t o[32];
@@ -500,7 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
         tmem_wait_ld();
 #pragma unroll
         for (int v = 0; v < 8; ++v)
-          __stcg(reinterpret_cast<float4*>(my_o + c * 32 + v * 4),
+          __stcg(my_o + (c * 8 + v) * kRowsWs,
                  make_float4(__uint_as_float(o[4 * v]), __uint_as_float(o[4 * v + 1]), __uint_as_float(o[4 * v + 2]),
                              __uint_as_float(o[4 * v + 3])));
       }
@@ -536,10 +545,10 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
 #pragma unroll
           for (int e = 0; e < 32; ++e) acc[e] = 0.f;
           for (int i = 0; i < ns; ++i) {
-            const float* src = p.ws_o + ((slot0 + i) * 2 * kBM + prow) * D + c * 32;
+            const float4* src = reinterpret_cast<const float4*>(p.ws_o) + (slot0 + i) * (D / 4) * kRowsWs + prow;
 #pragma unroll
             for (int v = 0; v < 8; ++v) {
-              const float4 x = __ldcg(reinterpret_cast<const float4*>(src + v * 4));
+              const float4 x = __ldcg(src + (c * 8 + v) * kRowsWs);
               acc[4 * v + 0] += mi[i] * x.x;
               acc[4 * v + 1] += mi[i] * x.y;
               acc[4 * v + 2] += mi[i] * x.z;
@@ -552,8 +561,10 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
     }
   }
 
+  if (stamp_end) DF_STAMP(warp == 4 ? 0 : 1, kTraceIters - 1, 7);
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) DF_STAMP(2, kTraceIters - 1, 8);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -1054,8 +1065,16 @@ namespace {
 // makespan over the SMs, charging a fixed prologue/epilogue cost per CTA and
 // a combine cost per split piece.  Cost unit: one 128-key tile for a full
 // pair of 128-row query tiles.
-constexpr double kPieceOverhead = 3.0;
-constexpr double kSplitOverhead = 2.0;
+double env_or(const char* name, double dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atof(v) : dflt;
+}
+const double kPieceOverhead = env_or("DF_PLAN_PIECE", 3.0);  // dev override for calibration sweeps
+const double kSplitOverhead = env_or("DF_PLAN_SPLIT", 1.0);
+// the last-arriving piece of a split pair reads every piece's fp32 partial
+// (128 KB each) alone: ~1 tile-unit per piece on that one CTA (calibrated with
+// scripts/plan_sweep.py: Wan all-context 880 -> 804 us, packed unchanged)
+const double kCombinePerPiece = env_or("DF_PLAN_COMBINE", 1.0);
 constexpr double kSingleTileFactor = 0.6;  // last pair with only its first tile valid
 constexpr int kMaxSplit = 16;
 
@@ -1084,7 +1103,8 @@ double simulate(const df_attn_args* a, const uint8_t* ns, const int* order, int 
       const double f = (qp == nq - 1 && last_single) ? kSingleTileFactor : 1.0;
       for (int s = 0; s < ns[h]; ++s) {
         const int len = ((s + 1) * tiles) / ns[h] - (s * tiles) / ns[h];
-        const double c = len * f + kPieceOverhead + (ns[h] > 1 ? kSplitOverhead : 0.0);
+        double c = len * f + kPieceOverhead + (ns[h] > 1 ? kSplitOverhead : 0.0);
+        if (ns[h] > 1 && s == ns[h] - 1) c += kCombinePerPiece * ns[h];  // (arrival order approximated)
         const double t0 = bins.top();
         bins.pop();
         bins.push(t0 + c);
