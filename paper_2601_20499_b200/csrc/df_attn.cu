@@ -1075,7 +1075,7 @@ const double kSplitOverhead = env_or("DF_PLAN_SPLIT", 1.0);
 // (128 KB each) alone: ~1 tile-unit per piece on that one CTA (calibrated with
 // scripts/plan_sweep.py: Wan all-context 880 -> 804 us, packed unchanged)
 const double kCombinePerPiece = env_or("DF_PLAN_COMBINE", 1.0);
-constexpr double kSingleTileFactor = 0.6;  // last pair with only its first tile valid
+constexpr double kSingleTileFactor = 0.95;  // last pair with only its first tile valid: no ping-pong, ~as slow as a full pair (clock64 trace)
 constexpr int kMaxSplit = 16;
 
 struct Plan {
