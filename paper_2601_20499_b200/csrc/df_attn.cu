@@ -95,6 +95,7 @@ struct __align__(64) AttnParams {
 // and the MMA issuer, first kTraceIters kv tiles.  Read with df_trace_fetch.
 constexpr int kTraceIters = 128;
 __device__ unsigned long long g_trace[3][kTraceIters][10];
+__device__ unsigned long long g_cta_time[1024][2];  // clock64 at CTA start / end (per-SM clocks)
 #define DF_STAMP(who, it, k)                                                        \
   do {                                                                              \
     if (blockIdx.x == 0 && (it) < kTraceIters) g_trace[who][it][k] = clock64();      \
@@ -189,6 +190,9 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
     fence_mbar_init();
   }
   if (threadIdx.x == 0) DF_STAMP(2, kTraceIters - 1, 6);
+#ifdef DF_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_time[blockIdx.x][0] = clock64();
+#endif
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
@@ -565,6 +569,9 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) DF_STAMP(2, kTraceIters - 1, 8);
+#ifdef DF_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_time[blockIdx.x][1] = clock64();
+#endif
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -1324,6 +1331,9 @@ extern "C" int df_attn_fwd(const df_attn_args* a, void* stream) {
 }
 
 #ifdef DF_TRACE
+extern "C" DF_API int df_trace_cta(void* host) {
+  return cudaMemcpyFromSymbol(host, dfb::g_cta_time, sizeof(dfb::g_cta_time)) == cudaSuccess ? DF_OK : DF_E_CUDA;
+}
 extern "C" DF_API int df_trace_fetch(void* host, int64_t bytes) {
   if (bytes > int64_t(sizeof(dfb::g_trace))) bytes = sizeof(dfb::g_trace);
   return cudaMemcpyFromSymbol(host, dfb::g_trace, bytes) == cudaSuccess ? DF_OK : DF_E_CUDA;

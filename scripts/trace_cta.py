@@ -15,7 +15,7 @@ work = [K.HeadWork(arena, arena.allocate(c), c, h, h) for h, c in enumerate(ctxs
 for _ in range(3):
     K.attention(q, out, work, hw, 1 / math.sqrt(D))
 torch.cuda.synchronize()
-buf = np.zeros((160, 2), dtype=np.uint64)
+buf = np.zeros((1024, 2), dtype=np.uint64)
 assert lib.df_trace_cta(buf.ctypes.data) == 0
 dur = (buf[:, 1].astype(np.int64) - buf[:, 0].astype(np.int64))
 plan = [l for l in open(os.environ.get("DUMP", "/dev/null")).read().splitlines() if l.startswith("cta ")][:148]
