@@ -75,7 +75,7 @@ struct __align__(64) AttnParams {
   const uint8_t* row_sampled;
   float* probe_rows;
   float* ws_o;           // split partials, unnormalised O: [slot][D/4][256] float4 (CTA pair: [slot][256][D])
-  float* ws_ml;          // [slot][256][2] (running max in log2 units, row sum)
+  float* ws_ml;          // [slot][256][8]: running max (log2 units), row sum, probe region masses
   int32_t* ws_cnt;       // [group] arrival counters (zero between launches)
   int64_t out_ld;
   int32_t hw;
@@ -517,7 +517,11 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
                  make_float4(__uint_as_float(o[4 * v]), __uint_as_float(o[4 * v + 1]), __uint_as_float(o[4 * v + 2]),
                              __uint_as_float(o[4 * v + 3])));
       }
-      __stcg(reinterpret_cast<float2*>(p.ws_ml + ((slot0 + piece) * 2 * kBM + prow) * 2), make_float2(m, l));
+      {  // (m, l) and, with the probe epilogue, the three region masses of this piece
+        float4* ml = reinterpret_cast<float4*>(p.ws_ml + ((slot0 + piece) * 2 * kBM + prow) * 8);
+        __stcg(ml, make_float4(m, l, reg_acc[0], reg_acc[1]));
+        if constexpr (kProbe) __stcg(ml + 1, make_float4(reg_acc[2], 0.f, 0.f, 0.f));
+      }
       __threadfence();
       const int nthreads = two ? 256 : 128;
       softmax_bar_sync(nthreads);
@@ -532,17 +536,32 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
         float mi[16], li[16];
         float M = -INFINITY;
         for (int i = 0; i < ns; ++i) {
-          const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml + ((slot0 + i) * 2 * kBM + prow) * 2));
+          const float4 ml = __ldcg(reinterpret_cast<const float4*>(p.ws_ml + ((slot0 + i) * 2 * kBM + prow) * 8));
           mi[i] = ml.x;
           li[i] = ml.y;
           M = fmaxf(M, ml.x);
         }
         float den = 0.f;
+        float reg[3] = {0.f, 0.f, 0.f};
         for (int i = 0; i < ns; ++i) {
           mi[i] = ex2(mi[i] - M);
           den += mi[i] * li[i];
+          if constexpr (kProbe) {
+            const float* ml = p.ws_ml + ((slot0 + i) * 2 * kBM + prow) * 8;
+            reg[0] += mi[i] * __ldcg(ml + 2);
+            reg[1] += mi[i] * __ldcg(ml + 3);
+            reg[2] += mi[i] * __ldcg(ml + 4);
+          }
         }
         const float inv = 1.f / den;
+        if constexpr (kProbe) {
+          if (p.row_sampled[row]) {  // profiler.py:118-129 region masses of the whole row
+            float* dst = p.probe_rows + (static_cast<int64_t>(h) * p.hw + row) * 3;
+            dst[0] = reg[0] * inv;
+            dst[1] = reg[1] * inv;
+            dst[2] = reg[2] * inv;
+          }
+        }
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
           float acc[32];
@@ -1253,7 +1272,7 @@ extern "C" int df_attn_workspace_bytes(const df_attn_args* a, int64_t* bytes) {
   if (rc != DF_OK) return rc;
   if (!bytes) return set_error(DF_E_ARG, "df_attn_workspace_bytes: null output");
   const bool pair = use_pair(a);
-  *bytes = get_plan(a, (a->flags & DF_ATTN_PROBE) == 0 || pair, pair).ws_bytes;
+  *bytes = get_plan(a, true, pair).ws_bytes;
   return DF_OK;
 }
 
@@ -1266,7 +1285,7 @@ extern "C" int df_attn_fwd(const df_attn_args* a, void* stream) {
 
   // Split plan; fall back to no splitting when the workspace cannot hold it.
   const bool pair = use_pair(a);
-  Plan plan = get_plan(a, !probe || pair, pair);  // the 1-CTA probe epilogue does not combine pieces
+  Plan plan = get_plan(a, true, pair);  // split pieces combine O, l and the probe region masses
   if (plan.ws_bytes > 0 && (!a->workspace || a->workspace_bytes < plan.ws_bytes ||
                             (reinterpret_cast<uintptr_t>(a->workspace) & 255)))
     plan = get_plan(a, false, pair);

@@ -75,3 +75,40 @@ def test_stale_rows_and_masked_tails(scale_q, pair):
                    arena.v[w.base_row:w.base_row + w.n_tok], scale)
         err = (out[h * hw:(h + 1) * hw].float() - ref).abs().max().item() / ref.abs().max().item()
         assert err <= 2e-2, (h, err)
+
+
+def test_probe_region_masses_with_split_kv():
+    """DF_ATTN_PROBE on a launch the planner splits (2 heads, 94 kv tiles, 4 items on 148 SMs):
+    the combine merges O, l and the three region masses of every piece (profiler.py:118-129)."""
+    from paper_2601_20499_b200 import kernels as K
+
+    torch.manual_seed(3)
+    dev = torch.device("cuda:0")
+    hw, width, slots = 300, 128, 40
+    ctxs = [hw * slots, hw * 17]
+    arena = K.KVArena(sum(K.KVArena.region_rows(c) for c in ctxs), width, dev)
+    arena.k.normal_()
+    arena.v.normal_()
+    H = len(ctxs)
+    q = (torch.randn(H * hw, width, device=dev) * 2.0).to(torch.bfloat16)
+    out = torch.empty(H * hw, width, device=dev, dtype=torch.bfloat16)
+    work = [K.HeadWork(arena, arena.allocate(c), c, h, h) for h, c in enumerate(ctxs)]
+    codes = torch.randint(0, 3, (H, slots), dtype=torch.uint8)
+    sampled = torch.zeros(hw, dtype=torch.uint8)
+    sampled[::3] = 1
+    probe = K.ProbeBuffers(codes.to(dev), sampled.to(dev), torch.zeros(H, hw, 3, device=dev))
+    scale = 1.0 / math.sqrt(width)
+    K.attention(q, out, work, hw, scale, probe=probe)
+    torch.cuda.synchronize()
+    for h, w in enumerate(work):
+        s = (q[h * hw:(h + 1) * hw].float() @ arena.k[w.base_row:w.base_row + w.n_tok].float().T) * scale
+        pmat = torch.softmax(s, dim=-1)
+        region = codes[h].to(dev).long().repeat_interleave(hw)[: w.n_tok]
+        want = torch.stack([pmat[:, region == r].sum(-1) for r in range(3)], dim=-1)
+        rows = sampled.bool().to(dev)
+        err = (probe.probe_rows[h][rows] - want[rows]).abs().max().item()
+        assert err <= 2e-3, (h, err)
+        assert bool((probe.probe_rows[h][~rows] == 0).all())
+        ref = pmat @ arena.v[w.base_row:w.base_row + w.n_tok].float()
+        oerr = (out[h * hw:(h + 1) * hw].float() - ref).abs().max().item() / ref.abs().max().item()
+        assert oerr <= 2e-2, (h, oerr)
