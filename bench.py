@@ -55,6 +55,14 @@ def peaks():
     return 1590.0, 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def sustained_peak(burst: float) -> float:
+    """bf16_tflops_sustained of MEASURED_PEAKS.json (cuBLAS back to back for 4 s), else the burst figure."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p)).get("bf16_tflops_sustained", burst))
+    return burst
+
+
 def layer_flops(ctxs):
     return 4 * D * HW * sum(ctxs)
 
@@ -481,7 +489,8 @@ def gpu_arm(args, ws, rank, local):
                      "frac": achieved / bf16_peak, "traffic": ncu_traffic(),
                      "traffic_unit": "bytes per launch (dram read+write, profiles/r1_attn_packed_ncu.json)",
                      "algorithmic_bytes": attn_alg_bytes(), "kernel": "df_attn_kernel<128,false>",
-                     "flops_per_launch": flops_packed, "peak_source": peak_kind},
+                     "flops_per_launch": flops_packed, "peak_source": peak_kind,
+                     "frac_vs_sustained": achieved / sustained_peak(bf16_peak)},
         "pack_roofline": {"bound": "hbm", "achieved": pack_gbs, "peak": hbm_peak, "unit": "GB/s",
                           "frac": pack_gbs / hbm_peak, "bytes": pack_bytes, "ms": min(pack_ms),
                           "kernel": "df_pack_kernel"},
