@@ -1,0 +1,86 @@
+// Microbenchmark: cycles per 128-column softmax row-tile (FFMA2 scale-sub, ex2 / poly,
+// FADD2 sum, F2FP pack, plus the FMNMX3 row max) with 1 or 2 warps per SM sub-partition,
+// i.e. the FMHA softmax with one query tile active (the groups alternate) vs both.
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "../../paper_2601_20499_b200/csrc/df_ptx.cuh"
+using namespace dfb;
+
+template <int EMU, bool MAX>
+__global__ void __launch_bounds__(256, 1) k(unsigned* out, const float* src, int iters, float sl2, uint32_t eu,
+                                            long long* cyc) {
+  uint32_t r[128];
+#pragma unroll
+  for (int i = 0; i < 128; ++i) r[i] = __float_as_uint(src[i * 256 + threadIdx.x]);
+  float2 sum2 = make_float2(0.f, 0.f);
+  uint32_t acc = 0;
+  float m = 0.5f;
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    if (MAX) m = fmaxf(m, row_max128(r) * sl2);
+    const float2 scale2 = make_float2(sl2, sl2);
+    const float2 negm2 = make_float2(-m, -m);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int c = q * 32 + 2 * i;
+        const float2 x = fma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
+        float2 e;
+        if (((c / 2) * EMU) % 8 < EMU)
+          e = exp2_poly2(x, eu);
+        else
+          e = make_float2(ex2(x.x), ex2(x.y));
+        sum2 = add2(sum2, e);
+        pk[i] = pack_bf16x2(e.x, e.y);
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc += pk[i];
+    }
+    m += 1e-7f * (acc & 1);
+#pragma unroll
+    for (int i = 0; i < 128; ++i) r[i] ^= (acc & 1);
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+  if (acc == 0x1234567u && sum2.x == 1.f) out[0] = acc;
+}
+
+template <int EMU, bool MAX>
+void run(unsigned* d, const float* src, long long* cyc, int sms) {
+  const int iters = 2000;
+  for (int threads : {128, 256}) {
+    k<EMU, MAX><<<sms, threads>>>(d, src, iters, 0.1f, 1u << 23, cyc);
+    k<EMU, MAX><<<sms, threads>>>(d, src, iters, 0.1f, 1u << 23, cyc);
+    cudaDeviceSynchronize();
+    long long h;
+    cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
+    const double per_tile = double(h) / iters;  // cycles per 128-col row tile per warp
+    printf("emu %d/8 max %d warps/SMSP %d: %.0f cycles per row-tile per warp (%.1f exps/clk/SM)\n", EMU, MAX,
+           threads / 128, per_tile, threads / 32 * 32 * 128 / per_tile);
+  }
+}
+
+int main() {
+  unsigned* d;
+  cudaMalloc(&d, 64);
+  float* src;
+  long long* cyc;
+  cudaMalloc(&cyc, 8 * 1024);
+  cudaMalloc(&src, 128 * 256 * 4);
+  {
+    static float h[128 * 256];
+    for (int i = 0; i < 128 * 256; ++i) h[i] = -0.001f * (i % 9973);
+    cudaMemcpy(src, h, sizeof(h), cudaMemcpyHostToDevice);
+  }
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  run<0, false>(d, src, cyc, sms);
+  run<0, true>(d, src, cyc, sms);
+  run<1, true>(d, src, cyc, sms);
+  run<2, true>(d, src, cyc, sms);
+  run<3, true>(d, src, cyc, sms);
+  run<4, true>(d, src, cyc, sms);
+  return 0;
+}
