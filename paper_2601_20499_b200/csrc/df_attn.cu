@@ -54,6 +54,13 @@ constexpr float kRescaleThreshold = 8.0f;  // log2 units
 // evenly): MUFU ex2 is 16/clk/SM, so at d=128 exponentials alone need 100% of
 // the tensor-pipe time of a 2 x 128-row tile pair without this offload.
 constexpr int kEmuNum = DF_EMU_NUM;
+// Scheduling fences in the softmax (df_ptx.cuh sched_fence): without them ptxas
+// hoists all 112 MUFU ex2 of a tile above the first P store, so the early
+// release of P's first half happens only after every exponential (1: fence
+// after the first-half release, 2: also after every other P quarter).
+#ifndef DF_SCHED_FENCE
+#define DF_SCHED_FENCE 1
+#endif
 __host__ __device__ constexpr bool emulated_pair(int i) { return (i * kEmuNum) % 8 < kEmuNum; }
 
 struct HeadParam {
@@ -432,11 +439,17 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
           }
         }
         tmem_st16(tS + quarter * 16, pk);
+#if DF_SCHED_FENCE >= 2
+        if (quarter != 1) sched_fence(p.n_heads < 0, last_flag);
+#endif
         if (quarter == 1) {  // release the first half of P early: PV can start on keys 0-63
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(p_full + 2 * t);
           if (stamp) DF_STAMP(t, jj, 4);
+#if DF_SCHED_FENCE
+          sched_fence(p.n_heads < 0, last_flag);  // keep the second half's exponentials below the release
+#endif
         }
       }
       if constexpr (kProbe) {
@@ -716,23 +729,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader CTA)
-    if (lane == 0 && crank == 0) {
+    // Warp-wide loop, elected lane issues, precomputed descriptor bases (as df_attn_kernel).
+    if (crank == 0) {
       constexpr uint32_t idesc_qk = idesc_bf16(2 * kBM, kBN, false);
       constexpr uint32_t idesc_pv = idesc_bf16(2 * kBM, D, true);
-      const uint32_t sQ = smem_u32(smem + C::kQOff);
-      const uint32_t sK = smem_u32(smem + C::kKOff);
-      const uint32_t sV = smem_u32(smem + C::kVOff);
+      const uint64_t dQ = sdesc_sw128(smem_u32(smem + C::kQOff), 16, 1024);
+      const uint64_t dK = sdesc_sw128(smem_u32(smem + C::kKOff), 16, 1024);
+      const uint64_t dV = sdesc_sw128(smem_u32(smem + C::kVOff), 16, 1024);
       const uint32_t tS0 = tmem, tS1 = tmem + 128;
       const uint32_t tO0 = tmem + C::kTmemO, tO1 = tmem + C::kTmemO + D;
 
       auto qk = [&](uint32_t d_tmem, int t, int ks) {
-        const uint32_t qa = sQ + t * C::kQTileBytes;
-        const uint32_t kb = sK + ks * C::kKHalfBytes;
+        const uint64_t qa = dQ + ((t * C::kQTileBytes) >> 4);
+        const uint64_t kb = dK + ((ks * C::kKHalfBytes) >> 4);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t oa = (kk >> 2) * C::kQBoxBytes + (kk & 3) * 32;
-          const uint32_t ob = (kk >> 2) * C::kKBoxBytes + (kk & 3) * 32;
-          umma_ss_pair(d_tmem, sdesc_sw128(qa + oa, 16, 1024), sdesc_sw128(kb + ob, 16, 1024), idesc_qk, kk > 0);
+          const uint64_t oa = ((kk >> 2) * C::kQBoxBytes + (kk & 3) * 32) >> 4;
+          const uint64_t ob = ((kk >> 2) * C::kKBoxBytes + (kk & 3) * 32) >> 4;
+          umma_ss_pair_elect(d_tmem, qa + oa, kb + ob, idesc_qk, kk > 0);
         }
       };
       auto pv = [&](int t, int jj) {
@@ -743,7 +757,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait_cluster(v_full + vs, (jj / C::kStages) & 1);
           tc_fence_after();
         }
-        const uint32_t vb = sV + vs * C::kVHalfBytes;
+        const uint64_t vb = dV + ((vs * C::kVHalfBytes) >> 4);
         const uint32_t tP = t ? tS1 : tS0;
         const uint32_t tO = t ? tO1 : tO0;
 #pragma unroll
@@ -752,28 +766,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_wait_cluster(p_full + 2 * t + 1, jj & 1);
             tc_fence_after();
           }
-          umma_ts_pair(tO, tP + kk * 8, sdesc_sw128(vb + kk * 2048, 16, 1024), idesc_pv,
-                       (jj > 0 || kk > 0) ? 1u : 0u);
+          umma_ts_pair_elect(tO, tP + kk * 8, vb + ((kk * 2048) >> 4), idesc_pv, (jj > 0 || kk > 0) ? 1u : 0u);
         }
-        umma_commit_pair(o_full + t);
-        if (t == 1 || !two) umma_commit_pair(v_empty + vs);
+        umma_commit_pair_elect(o_full + t);
+        if (t == 1 || !two) umma_commit_pair_elect(v_empty + vs);
       };
 
       mbar_wait_cluster(q_full, 0);
       tc_fence_after();
       for (int jj = 0; jj < n_kv; ++jj) {
         const int ks = jj % C::kStages;
+        if (lane == 0) DF_STAMP(2, jj, 0);
         mbar_wait_cluster(k_full + ks, (jj / C::kStages) & 1);
         tc_fence_after();
+        if (lane == 0) DF_STAMP(2, jj, 1);
         qk(tS0, 0, ks);
-        umma_commit_pair(s_full + 0);
+        umma_commit_pair_elect(s_full + 0);
         if (two) {
+          if (lane == 0) DF_STAMP(2, jj, 2);
           if (jj > 0) pv(1, jj - 1);
+          if (lane == 0) DF_STAMP(2, jj, 3);
           qk(tS1, 1, ks);
-          umma_commit_pair(s_full + 1);
+          umma_commit_pair_elect(s_full + 1);
         }
-        umma_commit_pair(k_empty + ks);
+        umma_commit_pair_elect(k_empty + ks);
+        if (lane == 0) DF_STAMP(2, jj, 4);
         pv(0, jj);
+        if (lane == 0) DF_STAMP(2, jj, 5);
       }
       if (two) pv(1, n_kv - 1);
     }
@@ -792,16 +811,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     float l = 0.f;
     float reg_acc[3] = {0.f, 0.f, 0.f};
 
+    const bool stamp = lane == 0 && quad == 0;
     for (int jj = 0; jj < n_kv; ++jj) {
       const int j = kv_begin + jj;
+      if (stamp) DF_STAMP(t, jj, 0);
       mbar_wait_cluster(s_full + t, jj & 1);
       tc_fence_after();
+      if (stamp) DF_STAMP(t, jj, 1);
       uint32_t r[128];
       tmem_ld32(tS + 0, r + 0);
       tmem_ld32(tS + 32, r + 32);
       tmem_ld32(tS + 64, r + 64);
       tmem_ld32(tS + 96, r + 96);
       tmem_wait_ld();
+      if (stamp) DF_STAMP(t, jj, 2);
       const int valid = hd.n_tok - j * kBN;
       if (valid < kBN) {
 #pragma unroll
@@ -809,6 +832,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (c >= valid) r[c] = __float_as_uint(-INFINITY);
       }
       const float m_tile = row_max128(r) * sl2;
+      if (stamp) DF_STAMP(t, jj, 3);
       if (jj == 0) {
         m = m_tile;
       } else {
@@ -890,6 +914,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           tc_fence_before();
           wg_bar_sync(2 + t);  // all 128 rows of this CTA's P half written
           if (row_local == 0) mbar_arrive_cluster(lp0);
+          if (stamp) DF_STAMP(t, jj, 4);
+#if DF_SCHED_FENCE
+          sched_fence(p.n_heads < 0, last_flag);
+#endif
         }
       }
       if constexpr (kProbe) {
@@ -910,6 +938,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_before();
       wg_bar_sync(2 + t);
       if (row_local == 0) mbar_arrive_cluster(lp1);
+      if (stamp) DF_STAMP(t, jj, 5);
     }
 
     // ------------------------------------------------------------ epilogue

@@ -282,6 +282,36 @@ __device__ __forceinline__ void umma_ts_pair(uint32_t d_tmem, uint32_t a_tmem, u
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// elected-lane forms for a warp-wide issuer loop (operands warp-uniform)
+__device__ __forceinline__ void umma_ss_pair_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                   uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_ts_pair_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                                   uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
 // arrive (when this thread's prior pair MMAs complete) on the barrier at this
 // smem offset in both CTAs of the pair
 __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
@@ -290,6 +320,16 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
           smem_u32(bar)),
       "h"(static_cast<uint16_t>(3))
       : "memory");
+}
+
+// Scheduling fence: ptxas does not move instructions across a clock read, so
+// reading %clock here pins the schedule at this point.  The value is kept live
+// by a store behind a launch-time-false branch (``never``), so the read is not
+// dead code; nothing is stored in practice.
+__device__ __forceinline__ void sched_fence(bool never, void* smem_word) {
+  uint32_t t;
+  asm volatile("mov.u32 %0, %%clock;" : "=r"(t)::"memory");
+  if (never) asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(smem_word)), "r"(t) : "memory");
 }
 
 // ---------------------------------------------------------------- math

@@ -6,6 +6,7 @@ from paper_2601_20499_b200 import kernels as K
 
 dev = torch.device('cuda:0')
 D = 128
+PAIR = os.environ.get("DF_PAIR") == "1"
 def run(ctxs, HW=4680, reps=20, probe=False):
     H = len(ctxs)
     arena = K.KVArena(sum(K.KVArena.region_rows(c) for c in ctxs), D, dev)
@@ -16,12 +17,12 @@ def run(ctxs, HW=4680, reps=20, probe=False):
     pb = None
     if probe:
         pb = K.ProbeBuffers(torch.zeros(H, 64, dtype=torch.uint8, device=dev), torch.ones(HW, dtype=torch.uint8, device=dev), torch.zeros(H, HW, 3, device=dev))
-    for _ in range(3): K.attention(q, out, work, HW, 1/math.sqrt(D), pb)
+    for _ in range(3): K.attention(q, out, work, HW, 1/math.sqrt(D), pb, pair=PAIR)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ts = []
     e0.record()
-    for _ in range(reps): K.attention(q, out, work, HW, 1/math.sqrt(D), pb)
+    for _ in range(reps): K.attention(q, out, work, HW, 1/math.sqrt(D), pb, pair=PAIR)
     e1.record(); torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / reps
     return t * 1e3, 4 * D * HW * sum(ctxs) / (t * 1e-3) / 1e12
