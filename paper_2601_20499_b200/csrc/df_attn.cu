@@ -682,8 +682,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(s_full + t, 1);
-      mbar_init(p_full + 2 * t, 2);  // one arrival per CTA of the pair
-      mbar_init(p_full + 2 * t + 1, 2);
+      mbar_init(p_full + 2 * t, 8);  // one arrival per softmax warp of either CTA
+      mbar_init(p_full + 2 * t + 1, 8);
       mbar_init(o_full + t, 1);
     }
     fence_mbar_init();
@@ -806,6 +806,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t tO = tmem + lane_off + C::kTmemO + t * D;
     const uint32_t lp0 = mapa_shared(smem_u32(p_full + 2 * t), 0);
     const uint32_t lp1 = mapa_shared(smem_u32(p_full + 2 * t + 1), 0);
+    auto arrive_p = [&](int half) {  // the leader's warps arrive locally, the peer's remotely
+      if (crank == 0)
+        mbar_arrive(p_full + 2 * t + half);
+      else
+        mbar_arrive_cluster(half ? lp1 : lp0);
+    };
     const float sl2 = p.scale_log2;
     float m = -INFINITY;
     float l = 0.f;
@@ -910,10 +916,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         tmem_st16(tS + quarter * 16, pk);
         if (quarter == 1) {
+          if (stamp) DF_STAMP(t, jj, 6);
           tmem_wait_st();
+          if (stamp) DF_STAMP(t, jj, 7);
           tc_fence_before();
-          wg_bar_sync(2 + t);  // all 128 rows of this CTA's P half written
-          if (row_local == 0) mbar_arrive_cluster(lp0);
+          __syncwarp();
+          if (stamp) DF_STAMP(t, jj, 8);
+          if (lane == 0) arrive_p(0);  // one arrival per warp: no named barrier on the P path
           if (stamp) DF_STAMP(t, jj, 4);
 #if DF_SCHED_FENCE
           sched_fence(p.n_heads < 0, last_flag);
@@ -936,8 +945,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       l += sum2.x + sum2.y;
       tmem_wait_st();
       tc_fence_before();
-      wg_bar_sync(2 + t);
-      if (row_local == 0) mbar_arrive_cluster(lp1);
+      __syncwarp();
+      if (lane == 0) arrive_p(1);
       if (stamp) DF_STAMP(t, jj, 5);
     }
 

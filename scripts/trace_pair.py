@@ -29,13 +29,17 @@ assert lib.df_trace_fetch(buf.ctypes.data, buf.nbytes) == 0
 t0 = int(buf[2, 0, 0])
 b = buf.astype(np.int64) - t0
 print("it | MMA: kwait qk0 | pv1(wait P1) | qk1 | pv0(wait P0) || SM0: wait S  ldtm  max  half  full || SM1: wait S ldtm max half full")
-for it in range(20, 44):
+for it in range(20, 30):
     m = b[2, it]
     s0, s1 = b[0, it], b[1, it]
     print(f"{it:3d} | {m[1]-m[0]:5d} {m[2]-m[1]:5d} | {m[3]-m[2]:5d} | {m[4]-m[3]:5d} | {m[5]-m[4]:5d} || "
           f"{s0[1]-s0[0]:5d} {s0[2]-s0[1]:5d} {s0[3]-s0[2]:5d} {s0[4]-s0[3]:5d} {s0[5]-s0[4]:5d} || "
           f"{s1[1]-s1[0]:5d} {s1[2]-s1[1]:5d} {s1[3]-s1[2]:5d} {s1[4]-s1[3]:5d} {s1[5]-s1[4]:5d}")
 per_it = (b[2, 100, 0] - b[2, 20, 0]) / 80
+print("pair softmax first half: max->exps(q0,q1) | wait_st | wg_bar | remote arrive")
+for it in range(20, 30):
+    s0 = b[0, it]
+    print(it, s0[6] - s0[3], s0[7] - s0[6], s0[8] - s0[7], s0[4] - s0[8])
 print("MMA loop period (cycles/iteration):", per_it, " ideal MMA at 8192 flop/clk:", 4 * 2 * 128 * 128 * 128 / 8192)
 print("absolute stamps it 30 (rel. MMA k-wait start):")
 for name, row in (("MMA", b[2, 30, :6]), ("SM0", b[0, 30, :6]), ("SM1", b[1, 30, :6])):
