@@ -130,7 +130,7 @@ struct AttnCfg {
   static constexpr int kKOff = kQOff + 2 * kTileBytes;
   static constexpr int kVOff = kKOff + kStagesK * kTileBytes;
   static constexpr int kBarOff = kVOff + kStagesV * kTileBytes;
-  static constexpr int kNumBars = 1 + 2 * kStagesK + 2 * kStagesV + 10;
+  static constexpr int kNumBars = 1 + 2 * kStagesK + 2 * kStagesV + 8;
   static constexpr int kSmem = kBarOff + kNumBars * 8 + 32 + 1024;  // + 1 KB alignment slack
   static constexpr uint32_t kTmemO = 256;
 };
@@ -1105,20 +1105,6 @@ static int launch_attn(const AttnParams& p, int grid, cudaStream_t stream) {
   return DF_OK;
 }
 
-}  // namespace dfb
-
-#include "df_attn_colsplit.cuh"
-#include "df_attn_db.cuh"
-
-namespace dfb {
-
-#ifndef DF_COLSPLIT
-#define DF_COLSPLIT 0
-#endif
-#ifndef DF_ATTN_DB
-#define DF_ATTN_DB 0
-#endif
-
 int sm_count_cached() {
   static int count = 0;
   static std::once_flag once;
@@ -1397,9 +1383,7 @@ extern "C" int df_attn_fwd(const df_attn_args* a, void* stream) {
   if (pair) return probe ? launch_attn_pair<true>(p, 2 * acc, s) : launch_attn_pair<false>(p, 2 * acc, s);
   const int grid = acc;
   if (a->head_dim == 128) {
-    if (probe) return launch_attn<128, true>(p, grid, s);
-    if (DF_ATTN_DB) return launch_attn_db<128>(p, grid, s);
-    return DF_COLSPLIT ? launch_attn_cs<128>(p, grid, s) : launch_attn<128, false>(p, grid, s);
+    return probe ? launch_attn<128, true>(p, grid, s) : launch_attn<128, false>(p, grid, s);
   }
   return probe ? launch_attn<64, true>(p, grid, s) : launch_attn<64, false>(p, grid, s);
 }
