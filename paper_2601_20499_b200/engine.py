@@ -339,6 +339,9 @@ class Session:
         # heads this process owns ([h0, h1) of every layer); head-parallel
         # subclasses narrow it and override the three collective hooks below.
         self.head_range = self._owned_heads()
+        # heads of every layer this process runs, ascending (head_range until a
+        # head-parallel rebalance gives each layer its own set)
+        self.layer_heads: list[list[int]] = [list(self.head_range) for _ in range(config.num_layers)]
         self.observer = observer
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.stream = stream
@@ -371,6 +374,9 @@ class Session:
     def _gather_scores(self, local: torch.Tensor) -> torch.Tensor:
         """(layers, h_local, 3) probe scores -> (layers, heads, 3) on every process."""
         return local
+
+    def _after_step(self, ar_step: int) -> None:
+        """Hook after a step's cache appends (head-parallel rebalancing)."""
 
     def _fresh_caches(self) -> list[list[HeadKVCache]]:
         cfg = self.config
@@ -414,8 +420,7 @@ class Session:
 
     def _classes_for_layer(self, layer: int) -> list[HeadClass]:
         h = self.config.num_heads
-        r = self.head_range
-        return list(self.assignment.classes[layer * h + r.start : layer * h + r.stop])
+        return [self.assignment.classes[layer * h + i] for i in self.layer_heads[layer]]
 
     def _layer_attention(self, layer, q, caches, current_blocks, probe=None):
         mode = self._effective_mode()
@@ -462,9 +467,12 @@ class Session:
 
     def _model_qkv(self, layer, x, ar, t):
         q, k, v = self.model.qkv(layer, x, ar, t)
-        r = self.head_range
-        if len(r) != self.config.num_heads:
-            q, k, v = q[r.start : r.stop], k[r.start : r.stop], v[r.start : r.stop]
+        heads = self.layer_heads[layer]
+        if len(heads) != self.config.num_heads:
+            if heads == list(range(heads[0], heads[-1] + 1)):
+                q, k, v = q[heads[0] : heads[-1] + 1], k[heads[0] : heads[-1] + 1], v[heads[0] : heads[-1] + 1]
+            else:
+                q, k, v = q[heads], k[heads], v[heads]
         return as_device_bf16(q, self.device), as_device_bf16(k, self.device), as_device_bf16(v, self.device)
 
     def _project(self, layer, x, ar, t):
@@ -482,7 +490,7 @@ class Session:
         caches = self.caches[layer]
         views = [c.pending_view(cfg.HW, cfg.head_dim, self.device) for c in caches]
         q = torch.empty(len(caches), cfg.HW, cfg.head_dim, dtype=torch.bfloat16, device=self.device)
-        into(layer, x, ar, t, q, [kv[0] for kv in views], [kv[1] for kv in views], heads=self.head_range,
+        into(layer, x, ar, t, q, [kv[0] for kv in views], [kv[1] for kv in views], heads=self.layer_heads[layer],
              stream=self.stream)
         return q, [FrameBlock(ar, k, v) for k, v in views]
 
@@ -539,6 +547,7 @@ class Session:
                     segs += self.shadow_caches[layer][h].append_segments(block, self.device)
         if segs:
             launch_segments(segs, s)
+        self._after_step(ar_step)
         self._frames.append(getattr(x, "f32", x))
         self._step_counters.append((ar_step, step_counters))
         self._kernel_calls_last = list(step_counters[-1].kernel_calls)

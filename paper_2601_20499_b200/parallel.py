@@ -75,9 +75,17 @@ def max_over_ranks(value: float, group=None, device=None) -> float:
 
 
 class HeadParallelSession(Session):
-    """A Session whose heads are sharded over the ranks of ``group``."""
+    """A Session whose heads are sharded over the ranks of ``group``.
 
-    def __init__(self, model, config: SessionConfig, mode: str = "baseline", group=None, **kw):
+    Until classification every rank owns a contiguous block of H/P heads of
+    every layer.  With ``rebalance`` (default) the step that classifies ends by
+    re-dealing each layer's heads to ranks by LPT over their post-
+    classification context lengths (``lpt_owners``) and moving the rings of
+    the heads that change owner once, rank to rank (``exchange_frames``).
+    """
+
+    def __init__(self, model, config: SessionConfig, mode: str = "baseline", group=None, rebalance: bool = True,
+                 **kw):
         if not dist.is_initialized():
             raise ConfigError("HeadParallelSession needs torch.distributed to be initialised")
         self.group = group
@@ -85,12 +93,169 @@ class HeadParallelSession(Session):
         self.rank = dist.get_rank(group)
         head_partition(config.num_heads, self.world, self.rank)  # validates divisibility
         super().__init__(model, config, mode, **kw)
+        self.rebalance = rebalance and self.shadow_caches is None
+        self.owners = None  # (layers, heads) owner table once rebalanced
+        self._history: list[int] | None = None
 
     def _owned_heads(self) -> range:
         return head_partition(self.config.num_heads, self.world, self.rank)
 
     def _gather_outputs(self, layer: int, outputs: torch.Tensor) -> torch.Tensor:
+        if self.owners is not None:
+            return gather_head_outputs_owned(outputs, self.owners[layer], self.group)
         return gather_head_outputs(outputs, self.group)
 
     def _gather_scores(self, local: torch.Tensor) -> torch.Tensor:
         return gather_head_scores(local, self.group)
+
+    def _classify(self) -> None:
+        self._history = list(self.caches[0][0].frame_ids)  # identical for every head under the baseline policy
+        super()._classify()
+
+    def _after_step(self, ar_step: int) -> None:
+        if self.rebalance and self.owners is None and self.assignment is not None:
+            self._rebalance(ar_step)
+
+    def _rebalance(self, frame_id: int) -> None:
+        """Move heads to their LPT owners after the classifying step's append."""
+        import numpy as np
+
+        from . import kernels as K
+        from .kv_cache import HeadKVCache, RingStorage, derive_policy, extension_window
+
+        cfg = self.config
+        L, H = cfg.num_layers, cfg.num_heads
+        ext = extension_window(self.assignment, cfg) if cfg.context_extension else None
+        pol = [[derive_policy(self.assignment.classes[l * H + h], cfg, extended_window=ext) for h in range(H)]
+               for l in range(L)]
+        old = contiguous_owners(L, H, self.world)
+        new = lpt_owners(np.array([[p.ring_slots for p in row] for row in pol]), self.world)
+        keep, send, recv = rebalance_plan(old, new, self.rank)
+
+        def kept(p) -> list[int]:  # rebuild under p, then the classifying step's append (kv_cache.py:187-201)
+            frames: list[int] = []
+            for f in self._history:
+                frames = p.retain(frames + [f])
+            return p.retain(frames + [frame_id])
+
+        h0 = self.head_range.start
+        sends = []
+        for l, h, dst in send:
+            c = self.caches[l][h - h0]
+            if c.frame_ids != kept(pol[l][h]):
+                raise ConfigError(f"layer {l} head {h}: ring frames {c.frame_ids} != {kept(pol[l][h])}")
+            for f in c.frame_ids:
+                rows = c.storage.rows(c.slot_of(f))
+                sends += [(dst, c.storage.arena.k[rows]), (dst, c.storage.arena.v[rows])]
+        incoming: dict[tuple[int, int], HeadKVCache] = {}
+        recvs = []
+        if recv:
+            rows_needed = sum(K.KVArena.region_rows(pol[l][h].ring_slots * cfg.HW) for l, h, _ in recv)
+            arena = K.KVArena(rows_needed, K.padded_width(cfg.head_dim), self.device)
+            for l, h, src in recv:
+                p = pol[l][h]
+                st = RingStorage(arena, arena.allocate(p.ring_slots * cfg.HW), p.ring_slots, cfg.HW, cfg.head_dim)
+                n = HeadKVCache(p, storage=st)
+                for slot, f in enumerate(kept(p)):
+                    n._slot_frame[slot] = f
+                    rows = st.rows(slot)
+                    recvs += [(src, arena.k[rows]), (src, arena.v[rows])]
+                incoming[(l, h)] = n
+        torch.cuda.synchronize(self.device)  # the rings' last append is on the session stream
+        exchange_frames(sends, recvs, self.group)
+        torch.cuda.synchronize(self.device)
+        heads = [[h for h in range(H) if new[l, h] == self.rank] for l in range(L)]
+        self.caches = [[incoming[(l, h)] if (l, h) in incoming else self.caches[l][h - h0] for h in heads[l]]
+                       for l in range(L)]
+        self.layer_heads = heads
+        self.owners = new
+        self.rebalance_stats = {"kept": len(keep), "sent": len(send), "received": len(recv),
+                                "bytes_sent": sum(t.numel() * t.element_size() for _, t in sends)}
+
+
+# ---------------------------------------------------------------------------
+# Post-classification LPT rebalancing (SURVEY.md 8(e)): after the one-shot
+# classification the heads of a layer cost very different amounts (a packed
+# dummy head attends to 2 frames, a neighbour head to W), so the contiguous
+# equal blocks of ``head_partition`` leave ranks idle at every per-layer
+# all-gather.  Every rank computes the same longest-processing-time owner
+# table from the policies, and the retained frames of the heads that change
+# owner move ONCE, rank to rank (NCCL P2P over NVLink on the GPU box).
+
+
+def lpt_owners(costs, world: int):
+    """Owner rank of every (layer, head): per layer, heads by decreasing cost
+    (lower index first on ties) go to the least-loaded rank (lowest rank on
+    ties).  Deterministic, so all ranks agree without a collective."""
+    import numpy as np
+
+    costs = np.asarray(costs)
+    if costs.ndim != 2:
+        raise ConfigError("costs must be (layers, heads)")
+    if world < 1:
+        raise ConfigError("world must be >= 1")
+    owners = np.zeros(costs.shape, dtype=np.int64)
+    for layer in range(costs.shape[0]):
+        load = [0] * world
+        for h in sorted(range(costs.shape[1]), key=lambda h: (-int(costs[layer, h]), h)):
+            r = min(range(world), key=lambda r: (load[r], r))
+            owners[layer, h] = r
+            load[r] += int(costs[layer, h])
+    return owners
+
+
+def contiguous_owners(layers: int, heads: int, world: int):
+    """The owner table of ``head_partition`` (before classification)."""
+    import numpy as np
+
+    per = heads // world
+    return np.tile(np.arange(heads, dtype=np.int64) // per, (layers, 1))
+
+
+def rebalance_plan(old_owners, new_owners, rank: int):
+    """(keep, send, recv) lists of this rank, each in global (layer, head) order:
+    keep = [(l, h)], send = [(l, h, dst)], recv = [(l, h, src)]."""
+    keep, send, recv = [], [], []
+    L, H = old_owners.shape
+    for layer in range(L):
+        for h in range(H):
+            o, n = int(old_owners[layer, h]), int(new_owners[layer, h])
+            if o == rank and n == rank:
+                keep.append((layer, h))
+            elif o == rank:
+                send.append((layer, h, n))
+            elif n == rank:
+                recv.append((layer, h, o))
+    return keep, send, recv
+
+
+def exchange_frames(sends, recvs, group=None) -> None:
+    """Point-to-point moves of frame rows: ``sends`` / ``recvs`` are lists of
+    (peer, tensor) in the same global order on both sides of every pair."""
+    ops = [dist.P2POp(dist.isend, t, peer, group) for peer, t in sends]
+    ops += [dist.P2POp(dist.irecv, t, peer, group) for peer, t in recvs]
+    if not ops:
+        return
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+
+
+def gather_head_outputs_owned(local: torch.Tensor, owners_layer, group=None) -> torch.Tensor:
+    """(n_local, HW, d) of this rank's heads (ascending head index) -> (H, HW, d)
+    in global head order, for an arbitrary owner vector (uneven counts are
+    padded to the largest block for the all-gather)."""
+    world = dist.get_world_size(group)
+    owners = [int(o) for o in owners_layer]
+    counts = [owners.count(r) for r in range(world)]
+    width = max(counts)
+    pad = local
+    if local.shape[0] < width:
+        pad = torch.cat([local, local.new_zeros((width - local.shape[0], *local.shape[1:]))])
+    g = _all_gather(pad, group)  # (P, width, HW, d)
+    slot = [0] * world
+    index = []
+    for o in owners:
+        index.append(o * width + slot[o])
+        slot[o] += 1
+    flat = g.reshape(world * width, *g.shape[2:])
+    return flat[torch.tensor(index, device=flat.device)]

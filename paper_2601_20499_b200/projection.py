@@ -93,20 +93,22 @@ class ProjectedModel:
             raise ShapeError(f"frame input {tuple(t.shape)} != ({self.HW}, {self.model_dim})")
         return ResidualStream(t)
 
-    def _w_heads(self, layer: int, heads: range) -> torch.Tensor:
-        if heads.start == 0 and heads.stop == self.num_heads:
+    def _w_heads(self, layer: int, heads: Sequence[int]) -> torch.Tensor:
+        """W_qkv rows of ``heads`` (any ascending head list: a head-parallel rank's share)."""
+        heads = tuple(heads)
+        if heads == tuple(range(self.num_heads)):
             return self.w_qkv[layer]
-        key = (layer, heads.start, heads.stop)
+        key = (layer, heads)
         w = self._head_slices.get(key)
         if w is None:
             D, d = self.model_dim, self.head_dim
-            rows = [self.w_qkv[layer][j * D + heads.start * d : j * D + heads.stop * d] for j in range(3)]
+            rows = [self.w_qkv[layer][j * D + h * d : j * D + (h + 1) * d] for j in range(3) for h in heads]
             w = torch.cat(rows, dim=0).contiguous()
             self._head_slices[key] = w
         return w
 
     def qkv_into(self, layer: int, x: ResidualStream, ar_step: int, denoise_step: int, q_out: torch.Tensor,
-                 k_dst: list[torch.Tensor], v_dst: list[torch.Tensor], heads: range | None = None,
+                 k_dst: list[torch.Tensor], v_dst: list[torch.Tensor], heads: Sequence[int] | None = None,
                  stream: torch.cuda.Stream | None = None) -> None:
         """Q of ``heads`` into ``q_out`` (heads, HW, d); their K/V into ``k_dst`` / ``v_dst`` views."""
         heads = range(self.num_heads) if heads is None else heads

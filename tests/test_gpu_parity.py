@@ -241,6 +241,10 @@ def test_head_parallel_session_world1_matches_session():
         assert a.assignment == b.assignment
         assert ra.kernel_calls_steady == rb.kernel_calls_steady
         assert ra.output_digest == rb.output_digest
+        # the post-classification LPT rebalance ran (one rank: every head kept)
+        assert b.owners is not None and (b.owners == 0).all()
+        assert b.rebalance_stats == {"kept": 8, "sent": 0, "received": 0, "bytes_sent": 0}
+        assert b.layer_heads == [[0, 1, 2, 3]] * 2
     finally:
         dist.destroy_process_group()
 

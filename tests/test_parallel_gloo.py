@@ -84,3 +84,82 @@ def test_partitions_validate():
         P.head_partition(12, 5, 0)
     with pytest.raises(df.ConfigError):
         P.stream_partition(3, 2, 2)
+
+
+def _costs(L=4, H=8, seed=3):
+    """Post-classification ring sizes of a planted-style assignment: packed dummy
+    2 slots, sink 2, neighbour W=6 (kv_cache.py policies)."""
+    rng = np.random.default_rng(seed)
+    return rng.choice([2, 2, 6], size=(L, H))
+
+
+def _rebalance_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        L, H, HW, d = 4, 8, 3, 4
+        costs = _costs(L, H)
+        old = P.contiguous_owners(L, H, world)
+        new = P.lpt_owners(costs, world)
+        keep, send, recv = P.rebalance_plan(old, new, rank)
+        # every (layer, head) ring holds costs[l, h] frames of distinct data
+        frame = lambda l, h, f: torch.full((HW, d), float(1000 * l + 10 * h + f))
+        sends = [(dst, frame(l, h, f).clone()) for l, h, dst in send for f in range(int(costs[l, h]))]
+        bufs = [(src, torch.zeros(HW, d)) for l, h, src in recv for f in range(int(costs[l, h]))]
+        P.exchange_frames(sends, bufs, None)
+        expect = [frame(l, h, f) for l, h, _ in recv for f in range(int(costs[l, h]))]
+        ok_move = all(torch.equal(b, e) for (_, b), e in zip(bufs, expect))
+        # uneven per-layer output gather in global head order
+        full = torch.randn(H, HW, d, generator=torch.Generator().manual_seed(5))
+        ok_gather = True
+        for layer in range(L):
+            mine = [h for h in range(H) if new[layer, h] == rank]
+            got = P.gather_head_outputs_owned(full[mine].clone(), new[layer])
+            ok_gather &= torch.equal(got, full)
+        out_q.put((rank, new.tolist(), keep, send, recv, ok_move, ok_gather))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_lpt_rebalance_world2():
+    """Post-classification rebalancing over 2 gloo ranks: both ranks derive the
+    same LPT owner table, every head is kept, or sent by its old owner and
+    received by its new one, the moved frames arrive intact, and the uneven
+    per-layer output gather restores global head order."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rebalance_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][1] == res[1][1]
+    for rank, _, keep, send, recv, ok_move, ok_gather in res:
+        assert ok_move and ok_gather
+    L, H = 4, 8
+    seen = sorted([(l, h) for r in res for l, h in r[2]] + [(l, h) for r in res for l, h, _ in r[3]])
+    assert seen == [(l, h) for l in range(L) for h in range(H)]
+    sent = sorted((l, h, res_rank, dst) for res_rank, _, _, send, _, _, _ in res for l, h, dst in send)
+    got = sorted((l, h, src, res_rank) for res_rank, _, _, _, recv, _, _ in res for l, h, src in recv)
+    assert sent == got
+
+
+def test_lpt_owners_balance():
+    costs = _costs(30, 12, seed=7)
+    for world in (1, 2, 4):
+        owners = P.lpt_owners(costs, world)
+        for layer in range(costs.shape[0]):
+            loads = [int(costs[layer][owners[layer] == r].sum()) for r in range(world)]
+            # LPT bound: the heaviest rank exceeds the lightest by at most the largest job
+            assert max(loads) - min(loads) <= costs[layer].max()
+            contiguous = [int(costs[layer][r * (12 // world):(r + 1) * (12 // world)].sum()) for r in range(world)]
+            assert max(loads) <= max(contiguous)
+    assert np.array_equal(P.lpt_owners(costs, 2), P.lpt_owners(costs.copy(), 2))  # deterministic
+    assert (P.lpt_owners(costs, 1) == 0).all()
+    with pytest.raises(df.ConfigError):
+        P.lpt_owners(costs[0], 2)
