@@ -71,6 +71,7 @@ extern "C" {
 #define DF_TMAP_BYTES 128   /* one CUtensorMap */
 #define DF_MAPS_PER_ARENA 3 /* K (128-row box), V (128-row box), K (64-row box) */
 #define DF_MAX_APPEND_SEGS 128
+#define DF_MAX_PEERS 7      /* peer output buffers of the fused head-output all-gather */
 
 /* df_attn_args.flags */
 #define DF_ATTN_PROBE 1u       /* fused DHP region-mass epilogue */
@@ -111,6 +112,16 @@ typedef struct df_attn_args {
    * leaves its counters at zero).  NULL or too small => no kv splitting. */
   void* workspace;
   int64_t workspace_bytes;
+  /* Fused head-output all-gather (head-parallel sessions, SURVEY 8(e) / 8(f)
+   * row 2; replaces the NCCL all-gather after engine.py:111-137 scatters the
+   * outputs): the epilogue also stores every output row, at the same offset
+   * as in `out`, into each of these buffers -- the other ranks' gathered-
+   * output buffers mapped into this process (CUDA IPC / symmetric memory),
+   * so the stores travel over NVLink as tiles finish.  The caller orders the
+   * peers' reads after the launch (a cross-rank barrier on the stream).
+   * NULL / 0 = none.  Not supported with DF_ATTN_PAIR. */
+  void* const* peer_out;  /* host array [n_peers] of device pointers */
+  int32_t n_peers;        /* <= DF_MAX_PEERS */
 } df_attn_args;
 
 /* A row-strided device copy: `rows` rows of `row_bytes` bytes. row_bytes and

@@ -30,6 +30,7 @@ DF_MAX_ARENAS = 4
 DF_TMAP_BYTES = 128
 DF_MAPS_PER_ARENA = 3
 DF_MAX_APPEND_SEGS = 128
+DF_MAX_PEERS = 7
 DF_ATTN_PROBE = 1
 DF_ATTN_PAIR = 2
 DF_ATTN_SINGLE_CTA = 4
@@ -76,6 +77,8 @@ class AttnArgs(ctypes.Structure):
         ("probe_rows", ctypes.c_void_p),
         ("workspace", ctypes.c_void_p),
         ("workspace_bytes", ctypes.c_int64),
+        ("peer_out", ctypes.POINTER(ctypes.c_void_p)),
+        ("n_peers", ctypes.c_int32),
     ]
 
 

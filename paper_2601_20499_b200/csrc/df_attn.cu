@@ -84,6 +84,8 @@ struct __align__(64) AttnParams {
   float* ws_o;           // split partials, unnormalised O: [slot][D/4][256] float4 (CTA pair: [slot][256][D])
   float* ws_ml;          // [slot][256][8]: running max (log2 units), row sum, probe region masses
   int32_t* ws_cnt;       // [group] arrival counters (zero between launches)
+  __nv_bfloat16* peer_out[DF_MAX_PEERS];  // fused all-gather: the same rows into every peer's buffer
+  int32_t n_peers;
   int64_t out_ld;
   int32_t hw;
   int32_t d_out;
@@ -479,7 +481,8 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
     const int prow = t * kBM + row_local;           // row within the pair
     const int row = qp * 2 * kBM + prow;            // row within the head
     const bool row_ok = row < p.hw;
-    __nv_bfloat16* orow = p.out + (static_cast<int64_t>(hd.o_head) * p.hw + row) * p.out_ld;
+    const int64_t orow_off = (static_cast<int64_t>(hd.o_head) * p.hw + row) * p.out_ld;
+    __nv_bfloat16* orow = p.out + orow_off;
     auto store_row = [&](const float* o, int c0, float scale) {
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
@@ -491,6 +494,8 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
           w.z = pack_bf16x2(o[v * 8 + 4] * scale, o[v * 8 + 5] * scale);
           w.w = pack_bf16x2(o[v * 8 + 6] * scale, o[v * 8 + 7] * scale);
           *reinterpret_cast<uint4*>(orow + col) = w;
+          for (int pi = 0; pi < p.n_peers; ++pi)  // fused all-gather: NVLink stores into the peers' buffers
+            *reinterpret_cast<uint4*>(p.peer_out[pi] + orow_off + col) = w;
         }
       }
     };
@@ -1281,6 +1286,14 @@ int validate(const df_attn_args* a) {
   if (a->hw < 1) return set_error(DF_E_SHAPE, "df_attn_fwd: hw must be >= 1");
   if (!a->q || !a->out || !a->heads || !a->kv_maps) return set_error(DF_E_ARG, "df_attn_fwd: null pointer");
   if (a->out_ld < a->d_out) return set_error(DF_E_SHAPE, "df_attn_fwd: out_ld < d_out");
+  if (a->n_peers < 0 || a->n_peers > DF_MAX_PEERS || (a->n_peers > 0 && !a->peer_out))
+    return set_error(DF_E_ARG, "df_attn_fwd: n_peers %d outside [0, %d] or peer_out missing", a->n_peers,
+                     DF_MAX_PEERS);
+  for (int i = 0; i < a->n_peers; ++i)
+    if (!a->peer_out[i] || (reinterpret_cast<uintptr_t>(a->peer_out[i]) & 15))
+      return set_error(DF_E_ARG, "df_attn_fwd: peer_out[%d] null or not 16-byte aligned", i);
+  if (a->n_peers > 0 && (a->flags & DF_ATTN_PAIR))
+    return set_error(DF_E_ARG, "df_attn_fwd: peer outputs are not supported by the CTA-pair kernel");
   if (a->q_rows < 1 || a->q_rows > INT32_MAX) return set_error(DF_E_SHAPE, "df_attn_fwd: bad q_rows");
   if ((reinterpret_cast<uintptr_t>(a->q) & 15) || (reinterpret_cast<uintptr_t>(a->out) & 15) || (a->out_ld % 8))
     return set_error(DF_E_ARG, "df_attn_fwd: q/out must be 16-byte aligned, out_ld a multiple of 8");
@@ -1335,6 +1348,8 @@ extern "C" int df_attn_fwd(const df_attn_args* a, void* stream) {
   std::memcpy(p.kvmap, a->kv_maps, static_cast<size_t>(a->num_arenas) * DF_MAPS_PER_ARENA * DF_TMAP_BYTES);
   p.out = static_cast<__nv_bfloat16*>(a->out);
   p.out_ld = a->out_ld;
+  p.n_peers = a->n_peers;
+  for (int i = 0; i < a->n_peers; ++i) p.peer_out[i] = static_cast<__nv_bfloat16*>(a->peer_out[i]);
   p.hw = a->hw;
   p.d_out = a->d_out;
   p.n_heads = a->num_heads;

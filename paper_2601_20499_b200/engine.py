@@ -14,7 +14,7 @@ from __future__ import annotations
 import hashlib
 import math
 from dataclasses import dataclass, field
-from typing import Callable
+from typing import Callable, Sequence
 
 import numpy as np
 import torch
@@ -138,16 +138,30 @@ def _q_rows(q_heads: torch.Tensor, H: int, hw: int, d: int, width: int, device) 
     return q.reshape(H * hw, width).contiguous()
 
 
+@dataclass(frozen=True)
+class OutputTarget:
+    """Where a layer's outputs land in a head-parallel session with the fused
+    all-gather: ``out`` is this rank's bf16 [total_heads * HW, d8] gathered
+    buffer, ``heads`` the global index of each local head, ``peers`` device
+    pointers of the other ranks' buffers of the same layout; the FMHA epilogue
+    stores every output row into all of them (df_attn_args.peer_out)."""
+
+    out: torch.Tensor
+    heads: Sequence[int]
+    peers: Sequence[int] = ()
+
+
 def _dispatch(q_heads, caches: list[HeadKVCache], current_blocks: list[FrameBlock], head_dim: int,
-              groups: list[list[int]], probe: ProbeRequest | None = None, stream=None, timed: bool = True):
+              groups: list[list[int]], probe: ProbeRequest | None = None, stream=None, timed: bool = True,
+              target: OutputTarget | None = None):
     """Stage current frames, check the logical groups, launch one ragged FMHA."""
     if stream is not None:
         with torch.cuda.stream(stream):
-            return _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, stream, timed)
-    return _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, None, timed)
+            return _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, stream, timed, target)
+    return _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, None, timed, target)
 
 
-def _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, stream, timed):
+def _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, stream, timed, target=None):
     H = len(caches)
     if len(current_blocks) != H:
         raise ShapeError(f"{len(current_blocks)} current blocks for {H} caches")
@@ -179,8 +193,13 @@ def _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, strea
     width = caches[0].storage.arena.width
     q2 = _q_rows(q_heads, H, hw, head_dim, width, device)
     d8 = ((head_dim + 7) // 8) * 8
-    out = torch.empty(H * hw, d8, dtype=torch.bfloat16, device=device)
-    work = [K.HeadWork(c.storage.arena, c.storage.base_row, n_tok[h], h, h) for h, c in enumerate(caches)]
+    if target is None:
+        out, o_heads, peers = torch.empty(H * hw, d8, dtype=torch.bfloat16, device=device), list(range(H)), None
+    else:
+        out, o_heads, peers = target.out, list(target.heads), list(target.peers)
+        if len(o_heads) != H or out.dim() != 2 or out.shape[1] != d8 or out.shape[0] % hw:
+            raise ShapeError(f"output target {tuple(out.shape)} / {len(o_heads)} heads do not fit {H} x {hw} x {d8}")
+    work = [K.HeadWork(c.storage.arena, c.storage.base_row, n_tok[h], h, o_heads[h]) for h, c in enumerate(caches)]
     pb = None
     if probe is not None:
         max_slots = max(c.storage.slots for c in caches)
@@ -192,7 +211,7 @@ def _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, strea
     s = stream if stream is not None else torch.cuda.current_stream(device)
     # build every launch first so the timed region holds no host work
     copies = K.prepare_copies([sg[:6] for sg in segs])
-    attn = K.prepare_attention(q2, out, work, hw, 1.0 / math.sqrt(head_dim), pb, None, s)
+    attn = K.prepare_attention(q2, out, work, hw, 1.0 / math.sqrt(head_dim), pb, None, s, peers)
     if timed:
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record(s)
@@ -207,20 +226,21 @@ def _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, strea
         lc._events = tuple(ev)
     lc.physical_launches = len(copies) + len(attn)
     del segs
-    o = out.view(H, hw, d8)
+    o = out.view(-1, hw, d8)
     if d8 != head_dim:
         o = o[..., :head_dim]
     return o, lc
 
 
 def baseline_step(q_heads, caches: list[HeadKVCache], current_blocks: list[FrameBlock], config: SessionConfig,
-                  *, stream=None, probe: ProbeRequest | None = None, timed: bool = True):
+                  *, stream=None, probe: ProbeRequest | None = None, timed: bool = True,
+                  target: OutputTarget | None = None):
     """Full-window attention for every head of one layer (engine.py:140-152)."""
     for c in caches:
         if c.policy.kind != "baseline_window":
             raise ConfigError(f"baseline_step got a {c.policy.kind} cache")
     return _dispatch(q_heads, caches, current_blocks, config.head_dim, [list(range(len(caches)))], probe, stream,
-                     timed)
+                     timed, target)
 
 
 def _class_groups(classes: list[HeadClass]) -> list[list[int]]:
@@ -228,16 +248,16 @@ def _class_groups(classes: list[HeadClass]) -> list[list[int]]:
 
 
 def hma_step(q_heads, caches, current_blocks, classes: list[HeadClass], config: SessionConfig, *, stream=None,
-             probe: ProbeRequest | None = None, timed: bool = True):
+             probe: ProbeRequest | None = None, timed: bool = True, target: OutputTarget | None = None):
     """Class-specific contexts; logically one call per class present (engine.py:161-174)."""
     if len(classes) != len(caches):
         raise AssignmentError(f"{len(classes)} classes for {len(caches)} heads in this layer")
     return _dispatch(q_heads, caches, current_blocks, config.head_dim, _class_groups(list(classes)), probe, stream,
-                     timed)
+                     timed, target)
 
 
 def packed_step(q_heads, caches, current_blocks, classes: list[HeadClass], config: SessionConfig, *, stream=None,
-                probe: ProbeRequest | None = None, timed: bool = True):
+                probe: ProbeRequest | None = None, timed: bool = True, target: OutputTarget | None = None):
     """Dummy+sink share one logical call, neighbors the other (engine.py:177-195)."""
     if not config.packing_enabled:
         raise ConfigError("packed_step requires packing_enabled")
@@ -245,7 +265,7 @@ def packed_step(q_heads, caches, current_blocks, classes: list[HeadClass], confi
         raise AssignmentError(f"{len(classes)} classes for {len(caches)} heads in this layer")
     ds = [h for h, c in enumerate(classes) if c is not HeadClass.NEIGHBOR]
     nb = [h for h, c in enumerate(classes) if c is HeadClass.NEIGHBOR]
-    return _dispatch(q_heads, caches, current_blocks, config.head_dim, [ds, nb], probe, stream, timed)
+    return _dispatch(q_heads, caches, current_blocks, config.head_dim, [ds, nb], probe, stream, timed, target)
 
 
 def expected_step_macs(config: SessionConfig, mode: str, history_frames: int,
@@ -422,14 +442,21 @@ class Session:
         h = self.config.num_heads
         return [self.assignment.classes[layer * h + i] for i in self.layer_heads[layer]]
 
+    def _output_target(self, layer: int) -> OutputTarget | None:
+        """Hook: where the layer's outputs land (head-parallel fused gather); None = a fresh tensor."""
+        return None
+
     def _layer_attention(self, layer, q, caches, current_blocks, probe=None):
         mode = self._effective_mode()
+        tgt = self._output_target(layer) if probe is None else None
         if mode == "baseline":
-            return baseline_step(q, caches, current_blocks, self.config, stream=self.stream, probe=probe)
+            return baseline_step(q, caches, current_blocks, self.config, stream=self.stream, probe=probe, target=tgt)
         classes = self._classes_for_layer(layer)
         if mode == "hma":
-            return hma_step(q, caches, current_blocks, classes, self.config, stream=self.stream, probe=probe)
-        return packed_step(q, caches, current_blocks, classes, self.config, stream=self.stream, probe=probe)
+            return hma_step(q, caches, current_blocks, classes, self.config, stream=self.stream, probe=probe,
+                            target=tgt)
+        return packed_step(q, caches, current_blocks, classes, self.config, stream=self.stream, probe=probe,
+                           target=tgt)
 
     def _classify(self) -> None:
         cfg = self.config

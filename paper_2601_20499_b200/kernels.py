@@ -10,6 +10,7 @@ import ctypes
 import math
 import os
 from dataclasses import dataclass
+from typing import Sequence
 
 import torch
 
@@ -125,13 +126,16 @@ def prepare_attention(
     probe: ProbeBuffers | None = None,
     pair: bool | None = None,
     stream: torch.cuda.Stream | None = None,
+    peer_out: Sequence[int] | None = None,
 ) -> list[PreparedLaunch]:
     """Build the launch(es) of one ragged attention over every head in ``work``.
 
     ``q``: bf16 [q_heads*hw, width] (width = arena width); ``out``: bf16
     [o_heads*hw, d_out] with row stride ``out.stride(0)``.  One launch carries
     <= DF_MAX_HEADS heads from <= DF_MAX_ARENAS arenas; longer lists split into
-    contiguous runs (a session uses one arena: one launch).
+    contiguous runs (a session uses one arena: one launch).  ``peer_out``:
+    device pointers of buffers laid out like ``out`` (other ranks' gathered
+    outputs) that receive the same rows -- the fused head-output all-gather.
     """
     if not work:
         return []
@@ -151,7 +155,7 @@ def prepare_attention(
             sub_probe = None
             if probe is not None:
                 sub_probe = ProbeBuffers(probe.region_of_slot[sl], probe.row_sampled, probe.probe_rows[sl])
-            out_launches += prepare_attention(q, out, work[sl], hw, scale, sub_probe, pair, stream)
+            out_launches += prepare_attention(q, out, work[sl], hw, scale, sub_probe, pair, stream, peer_out)
         return out_launches
     if q.dtype != torch.bfloat16 or out.dtype != torch.bfloat16:
         raise ShapeError("q and out must be bfloat16")
@@ -201,6 +205,13 @@ def prepare_attention(
         args.region_of_slot = probe.region_of_slot.data_ptr()
         args.row_sampled = probe.row_sampled.data_ptr()
         args.probe_rows = probe.probe_rows.data_ptr()
+    peers = None
+    if peer_out:
+        if len(peer_out) > _lib.DF_MAX_PEERS:
+            raise ShapeError(f"{len(peer_out)} peer outputs > {_lib.DF_MAX_PEERS}")
+        peers = (ctypes.c_void_p * len(peer_out))(*peer_out)
+        args.peer_out = ctypes.cast(peers, ctypes.POINTER(ctypes.c_void_p))
+        args.n_peers = len(peer_out)
     need = ctypes.c_int64(0)
     _lib.call("df_attn_workspace_bytes", ctypes.byref(args), ctypes.byref(need))
     ws = None
@@ -208,7 +219,7 @@ def prepare_attention(
         ws = _split_workspace(q.device, _stream_handle(stream).value, need.value)
         args.workspace = ws.data_ptr()
         args.workspace_bytes = ws.numel()
-    return [PreparedLaunch("df_attn_fwd", (ctypes.byref(args),), (args, descs, maps_buf, ws, q, out, probe))]
+    return [PreparedLaunch("df_attn_fwd", (ctypes.byref(args),), (args, descs, maps_buf, ws, q, out, probe, peers))]
 
 
 def attention(

@@ -85,7 +85,7 @@ class HeadParallelSession(Session):
     """
 
     def __init__(self, model, config: SessionConfig, mode: str = "baseline", group=None, rebalance: bool = True,
-                 **kw):
+                 fused_gather: bool = False, **kw):
         if not dist.is_initialized():
             raise ConfigError("HeadParallelSession needs torch.distributed to be initialised")
         self.group = group
@@ -96,11 +96,28 @@ class HeadParallelSession(Session):
         self.rebalance = rebalance and self.shadow_caches is None
         self.owners = None  # (layers, heads) owner table once rebalanced
         self._history: list[int] | None = None
+        self.fused = None
+        if fused_gather:
+            d8 = ((config.head_dim + 7) // 8) * 8
+            self.fused = FusedHeadGather(config.num_heads * config.HW, d8, group, self.device)
+
+    def _output_target(self, layer: int):
+        if self.fused is None:
+            return None
+        return self.fused.target(layer, self.layer_heads[layer])
 
     def _owned_heads(self) -> range:
         return head_partition(self.config.num_heads, self.world, self.rank)
 
     def _gather_outputs(self, layer: int, outputs: torch.Tensor) -> torch.Tensor:
+        if self.fused is not None and outputs.data_ptr() == self.fused.buffer(layer).data_ptr():
+            # every rank's FMHA epilogue stored its heads' rows into all buffers
+            if self.stream is not None:
+                with torch.cuda.stream(self.stream):
+                    self.fused.barrier(layer)
+            else:
+                self.fused.barrier(layer)
+            return outputs[:, :, : self.config.head_dim]
         if self.owners is not None:
             return gather_head_outputs_owned(outputs, self.owners[layer], self.group)
         return gather_head_outputs(outputs, self.group)
@@ -259,3 +276,42 @@ def gather_head_outputs_owned(local: torch.Tensor, owners_layer, group=None) -> 
         slot[o] += 1
     flat = g.reshape(world * width, *g.shape[2:])
     return flat[torch.tensor(index, device=flat.device)]
+
+
+class FusedHeadGather:
+    """Gathered head-output buffers for the fused all-gather.
+
+    Two bf16 [total_heads * HW, d8] buffers per rank in symmetric memory
+    (torch.distributed._symmetric_memory: the allocation and the mapping of
+    every rank's buffer into every process), alternating by layer.  The FMHA
+    epilogue of each rank stores its heads' rows into its own buffer and, over
+    NVLink, into the peers' (df_attn_args.peer_out), so the gather overlaps the
+    attention tile by tile and no NCCL all-gather runs.  ``barrier(layer)``
+    (a device-side signal/wait on the stream) orders the peers' stores before
+    this rank reads the buffer; alternating buffers keep layer l+1's stores
+    off the buffer a slower rank may still be reading for layer l.
+    """
+
+    def __init__(self, rows: int, width: int, group, device):
+        import torch.distributed._symmetric_memory as symm
+
+        name = group.group_name if group is not None else dist.group.WORLD.group_name
+        self.bufs, self.handles, self.peers = [], [], []
+        for _ in range(2):
+            t = symm.empty((rows, width), dtype=torch.bfloat16, device=device)
+            h = symm.rendezvous(t, name)
+            peers = [h.get_buffer(r, tuple(t.shape), t.dtype).data_ptr() for r in range(h.world_size) if r != h.rank]
+            self.bufs.append(t)
+            self.handles.append(h)
+            self.peers.append(peers)
+
+    def buffer(self, layer: int) -> torch.Tensor:
+        return self.bufs[layer % 2]
+
+    def target(self, layer: int, heads):
+        from .engine import OutputTarget
+
+        return OutputTarget(self.bufs[layer % 2], list(heads), self.peers[layer % 2])
+
+    def barrier(self, layer: int) -> None:
+        self.handles[layer % 2].barrier(channel=0)

@@ -249,6 +249,71 @@ def test_head_parallel_session_world1_matches_session():
         dist.destroy_process_group()
 
 
+def test_fused_gather_peer_outputs_kernel():
+    """df_attn_args.peer_out: every output row is also stored into the peer
+    buffers (here a second local buffer stands in for a peer's mapping), on the
+    direct and the split-KV (in-kernel combine) epilogues, bit-identical to
+    the local rows; rows of heads this launch does not own stay untouched."""
+    from paper_2601_20499_b200 import kernels as K
+
+    torch.manual_seed(4)
+    hw, width = 300, 128
+    ctxs = [600, 4680 * 6 + 77, 1000]  # the long head splits its kv range
+    arena = K.KVArena(sum(K.KVArena.region_rows(c) for c in ctxs), width, DEV)
+    arena.k.normal_()
+    arena.v.normal_()
+    q = torch.randn(len(ctxs) * hw, width, device=DEV).to(torch.bfloat16)
+    total = 5  # gathered layout: global heads 4, 0, 2 of 5
+    o_heads = [4, 0, 2]
+    work = [K.HeadWork(arena, arena.allocate(c), c, h, o) for h, (c, o) in enumerate(zip(ctxs, o_heads))]
+    ref = torch.empty(len(ctxs) * hw, width, device=DEV, dtype=torch.bfloat16)
+    K.attention(q, ref, [K.HeadWork(w.arena, w.base_row, w.n_tok, w.q_head, h) for h, w in enumerate(work)], hw,
+                1 / math.sqrt(width))
+    mine = torch.full((total * hw, width), 7.0, device=DEV, dtype=torch.bfloat16)
+    peer = torch.full((total * hw, width), 7.0, device=DEV, dtype=torch.bfloat16)
+    for launch in K.prepare_attention(q, mine, work, hw, 1 / math.sqrt(width), peer_out=[peer.data_ptr()]):
+        launch.launch(None)
+    torch.cuda.synchronize()
+    assert torch.equal(mine, peer)
+    for h, o in enumerate(o_heads):
+        assert torch.equal(mine[o * hw:(o + 1) * hw], ref[h * hw:(h + 1) * hw])
+    for o in (1, 3):
+        assert (mine[o * hw:(o + 1) * hw] == 7.0).all()
+
+
+def test_head_parallel_fused_gather_world1_matches_session():
+    """HeadParallelSession(fused_gather=True): outputs go straight into the
+    symmetric-memory gathered buffer (global head rows) with the device
+    barrier instead of the NCCL all-gather; same result as the plain session."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2601_20499_b200.parallel import HeadParallelSession
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    try:
+        ocfg = O.Config(num_layers=3, num_heads=4, head_dim=64, HW=192, window_len=4, ar_steps=5, denoise_steps=1,
+                        dummy_count=3, probe_ar_step=2)
+        labels = ("sink", "neighbor", "current", "neighbor", "current", "sink", "neighbor", "current",
+                  "sink", "current", "neighbor", "sink")
+        stream = O.PlantedStream(labels, 2.0, O.derive(3, "planted"), ocfg)
+        cfg = df.SessionConfig(**ocfg.__dict__)
+        fa, ra = df.Session(stream, cfg, "packed").run()
+        b = HeadParallelSession(stream, cfg, "packed", fused_gather=True)
+        fb, rb = b.run()
+        assert b.fused is not None and b.fused.peers == [[], []]
+        assert ra.output_digest == rb.output_digest
+        assert ra.kernel_calls_steady == rb.kernel_calls_steady
+    finally:
+        dist.destroy_process_group()
+
+
 def test_step_graph_replay_matches_eager():
     """CUDA-graph capture of a denoise iteration: replays are
     bitwise equal to the eager public-API step, with fresh inputs each replay."""
