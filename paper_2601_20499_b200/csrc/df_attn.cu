@@ -494,8 +494,10 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
           w.z = pack_bf16x2(o[v * 8 + 4] * scale, o[v * 8 + 5] * scale);
           w.w = pack_bf16x2(o[v * 8 + 6] * scale, o[v * 8 + 7] * scale);
           *reinterpret_cast<uint4*>(orow + col) = w;
+#ifndef DF_NO_PEERS
           for (int pi = 0; pi < p.n_peers; ++pi)  // fused all-gather: NVLink stores into the peers' buffers
             *reinterpret_cast<uint4*>(p.peer_out[pi] + orow_off + col) = w;
+#endif
         }
       }
     };
