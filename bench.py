@@ -361,6 +361,97 @@ def full_layer(df, cfg, packed, classes, dev, gen, args, ws, bf16_peak):
 
 
 # ------------------------------------------------------------------ CPU leg
+def kernel_configs(df, dev, bf16_peak):
+    """Single-launch FMHA timings of the other configs SURVEY 8(d) names (CUDA events, median of 10 after
+    3 warm-ups, fresh K/V per config): 3d/4s/5n, N(0,3) logits (lazy rescaling is data dependent),
+    and the C4 high-resolution frame (HW 18720) packed and all-context."""
+    import math
+
+    import torch
+
+    from paper_2601_20499_b200 import kernels as K
+
+    def one(ctxs, hw, q_std=1.0):
+        arena = K.KVArena(sum(K.KVArena.region_rows(c) for c in ctxs), D, dev)
+        arena.k.normal_()
+        arena.v.normal_()
+        q = (torch.randn(len(ctxs) * hw, D, device=dev) * q_std).to(torch.bfloat16)
+        out = torch.empty(len(ctxs) * hw, D, device=dev, dtype=torch.bfloat16)
+        work = [K.HeadWork(arena, arena.allocate(c), c, h, h) for h, c in enumerate(ctxs)]
+        launches = K.prepare_attention(q, out, work, hw, 1 / math.sqrt(D))
+        for _ in range(3):
+            for l in launches:
+                l.launch(None)
+        ts = []
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for l in launches:
+                l.launch(None)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        us = sorted(ts)[len(ts) // 2] * 1e3
+        tf = 4 * D * hw * sum(ctxs) / (us * 1e-6) / 1e12
+        del arena, q, out
+        torch.cuda.empty_cache()
+        return {"us_per_layer": us, "tflops": tf, "frac": tf / bf16_peak}
+
+    hr = 4 * HW
+    res = {
+        "packed_3d4s5n": one([2 * HW] * 7 + [6 * HW] * 5, HW),
+        "packed_6d3s3n_logit_std3": one(PACKED_CTX, HW, 3.0),
+        "hires_c4_packed_6d3s3n": one([2 * hr] * 9 + [6 * hr] * 3, hr),
+        "hires_c4_all_context": one([7 * hr] * 12, hr),
+    }
+    res["hires_c4_speedup_packed_vs_all_context"] = (res["hires_c4_all_context"]["us_per_layer"]
+                                                     / res["hires_c4_packed_6d3s3n"]["us_per_layer"])
+    res["timing"] = "single launch, CUDA events, median of 10 (burst clocks)"
+    return res
+
+
+def rollout_c3(df, dev, ar_steps=40):
+    """BASELINE configs[2]: a whole Wan-shape rollout through the public Session -- fused QKV projection ->
+    FMHA -> out-projection per layer, probe with the DHP epilogue at AR step 2 (ratio 0.25), greedy
+    classification of 180 of the 360 heads as dummies, one df_kv_pack, then packed attention to the end
+    (40 AR steps = 120 latent frames).  Random-init weights of the Wan attention shape, synthetic frames."""
+    import torch
+
+    Dm = H * D
+    g = torch.Generator(device=dev).manual_seed(11)
+    weights = [{n: torch.randn(Dm, Dm, device=dev, generator=g) * (0.5 / Dm ** 0.5) for n in ("q", "k", "v", "o")}
+               for _ in range(L)]
+    frames = lambda ar, t: torch.randn(HW, Dm, device=dev, generator=g)
+    model = df.ProjectedModel(weights, frames, H, D, HW, device=dev)
+    cfg = df.SessionConfig(num_layers=L, num_heads=H, head_dim=D, HW=HW, window_len=W, ar_steps=ar_steps,
+                           denoise_steps=DENOISE, dummy_count=L * H // 2, probe_ar_step=2, subsample_ratio=0.25)
+    def run(graphs):
+        sess = df.Session(model, cfg, "packed", device=dev, graphs=graphs)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        frames_out, report = sess.run()
+        e1.record()
+        torch.cuda.synchronize()
+        del frames_out
+        return sess, report, e0.elapsed_time(e1)
+
+    sess, report, ms = run(False)
+    n_dummy = sum(c is df.HeadClass.DUMMY for c in sess.assignment.classes)
+    steady = [st["wall_time_ns"] for st in report.steps[W + 1:]]
+    res = {"latent_frames": ar_steps * FRAMES_PER_STEP, "ms": ms,
+           "fps": ar_steps * FRAMES_PER_STEP / (ms * 1e-3),
+           "dummy_heads": n_dummy, "pack_gb": (sess.pack_stats or {}).get("bytes", 0) / 1e9,
+           "cache_reduction_ratio": report.cache_reduction_ratio,
+           "attn_ms_per_step_steady": sum(steady) / len(steady) / 1e6 if steady else None,
+           "path": "Session.run(): per layer df_qkv_project -> df_attn_fwd -> df_out_project; probe (DHP epilogue) + "
+                   "classify + df_kv_pack inside the timed region; device-timed (CUDA events)"}
+    del sess
+    del model, weights
+    torch.cuda.empty_cache()
+    return res
+
+
 def cpu_sample(reps: int = 1):
     """Oracle port (engine.py:87-137, fp64 numpy) on 1 neighbor + 1 sink + 1 dummy head of one warm layer."""
     import numpy as np
@@ -469,6 +560,10 @@ def gpu_arm(args, ws, rank, local):
     launches = sum(lc.physical_launches for step in lcs for lc in step)
 
     fused = full_layer(df, cfg, packed, classes, dev, gen, args, ws, bf16_peak)
+    extra = {}
+    if not args.no_configs:
+        extra = kernel_configs(df, dev, bf16_peak)
+        extra["rollout_c3"] = rollout_c3(df, dev)
 
     # e2e through the public API with host buffers
     pinned = [tuple(x.cpu().pin_memory() for x in layer) for layer in inputs]
@@ -552,6 +647,7 @@ def gpu_arm(args, ws, rank, local):
                 "path": "public packed_step per layer; pinned host Q/K/V H2D on a copy stream (double-buffered), "
                         "outputs D2H on a second stream, all inside the timed region"},
         "layer_fused": fused,
+        "configs": extra,
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
@@ -568,6 +664,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-configs", action="store_true", help="skip the configs[2..3] / SURVEY 8(d) extra timings")
     args = ap.parse_args()
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))

@@ -304,8 +304,17 @@ class RunReport:
     kernel_calls_steady: list[int]
     total_key_token_macs: int
     total_wall_time_ns: int
-    output_digest: str
     physical_launches_steady: list[int] = field(default_factory=list)
+    frames: list = field(default_factory=list, repr=False, compare=False)
+    _digest: str | None = field(default=None, repr=False, compare=False)
+
+    @property
+    def output_digest(self) -> str:
+        """sha256 over the step outputs (engine.py report digest), computed on first access: it
+        reads every frame back to the host, which a rollout's timing should not include."""
+        if self._digest is None:
+            self._digest = _digest(self.frames)
+        return self._digest
 
     def to_dict(self) -> dict:
         return {
@@ -345,7 +354,8 @@ class Session:
 
     def __init__(self, model, config: SessionConfig, mode: str = "baseline",
                  observer: Callable[[StepTrace], None] | None = None, shadow: bool = False,
-                 device: torch.device | str | None = None, stream: torch.cuda.Stream | None = None):
+                 device: torch.device | str | None = None, stream: torch.cuda.Stream | None = None,
+                 graphs: bool = False):
         if mode not in MODES:
             raise ConfigError(f"unknown mode {mode!r}, expected one of {MODES}")
         if mode == "packed" and not config.packing_enabled:
@@ -382,6 +392,13 @@ class Session:
         self.caches = self._fresh_caches()
         self._shadow = shadow and mode != "baseline"
         self.shadow_caches = self._fresh_caches() if self._shadow else None
+        # CUDA-graph replay of whole denoise iterations: one graph per cache
+        # signature (pending slots + context lengths), captured on first use, all sharing one pool
+        self.graphs = graphs
+        self._graph_cache: dict[tuple, tuple] = {}
+        self._graph_pool = None
+        self._capture_stream: torch.cuda.Stream | None = None
+        self.graph_stats = {"captured": 0, "replayed": 0}
 
     def _owned_heads(self) -> range:
         return range(self.config.num_heads)
@@ -446,17 +463,76 @@ class Session:
         """Hook: where the layer's outputs land (head-parallel fused gather); None = a fresh tensor."""
         return None
 
-    def _layer_attention(self, layer, q, caches, current_blocks, probe=None):
+    def _layer_attention(self, layer, q, caches, current_blocks, probe=None, timed: bool = True):
         mode = self._effective_mode()
         tgt = self._output_target(layer) if probe is None else None
+        kw = dict(stream=self.stream, probe=probe, target=tgt, timed=timed)
         if mode == "baseline":
-            return baseline_step(q, caches, current_blocks, self.config, stream=self.stream, probe=probe, target=tgt)
+            return baseline_step(q, caches, current_blocks, self.config, **kw)
         classes = self._classes_for_layer(layer)
         if mode == "hma":
-            return hma_step(q, caches, current_blocks, classes, self.config, stream=self.stream, probe=probe,
-                            target=tgt)
-        return packed_step(q, caches, current_blocks, classes, self.config, stream=self.stream, probe=probe,
-                           target=tgt)
+            return hma_step(q, caches, current_blocks, classes, self.config, **kw)
+        return packed_step(q, caches, current_blocks, classes, self.config, **kw)
+
+    # ------------------------------------------------------------ CUDA graphs
+    def _graphable(self, ratios) -> bool:
+        """A denoise iteration can be captured: projected model (device-only, in-place residual),
+        no probe epilogue, no per-layer observer or shadow caches."""
+        return (self.graphs and not ratios and self.observer is None and self.shadow_caches is None
+                and hasattr(self.model, "qkv_into") and hasattr(self.model, "mix_into"))
+
+    def _layers(self, x, ar_step: int, t: int, timed: bool):
+        """One denoise iteration over every layer; returns (x, blocks per layer, counters)."""
+        counters = StepCounters()
+        blocks_all = []
+        for layer in range(self.config.num_layers):
+            q, blocks = self._project(layer, x, ar_step, t)
+            outputs, lc = self._layer_attention(layer, q, self.caches[layer], blocks, None, timed)
+            counters.add_layer(lc)
+            blocks_all.append(blocks)
+            x = self._mix(layer, outputs, x)
+        return x, blocks_all, counters
+
+    def _graph_iteration(self, x_in, ar_step: int, t: int):
+        """Replay (capturing on first use) the iteration graph of the current cache signature.
+
+        The graph is a function of the slot tables only: every denoise iteration of an AR step, and
+        every AR step whose pending slots repeat (the ring cycles), replays the same one.  ``x_in``
+        is copied into the graph's static residual buffers; the result lands there in place.
+        """
+        HW = self.config.HW
+        key = (self._effective_mode(), id(self.caches),
+               tuple((c.pending_slot, c.context_tokens(HW)) for row in self.caches for c in row))
+        entry = self._graph_cache.get(key)
+        s = self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
+        if entry is None:
+            if self._capture_stream is None:
+                self._capture_stream = torch.cuda.Stream(self.device)
+                self._graph_pool = torch.cuda.graph_pool_handle()
+            cs = self._capture_stream
+            x_static = type(x_in)(x_in.f32.clone(), x_in.bf16.clone())
+            cs.wait_stream(s)
+            saved, self.stream = self.stream, cs
+            try:
+                with torch.cuda.stream(cs):  # eager warm-up on the capture stream: its split workspace, error paths
+                    x_out, blocks_all, counters = self._layers(x_static, ar_step, t, timed=False)
+                s.wait_stream(cs)
+                g = torch.cuda.CUDAGraph()
+                x_cap = type(x_in)(x_in.f32.clone(), x_in.bf16.clone())
+                with torch.cuda.graph(g, stream=cs, pool=self._graph_pool):
+                    self._layers(x_cap, ar_step, t, timed=False)
+            finally:
+                self.stream = saved
+            self._graph_cache[key] = (g, x_cap, blocks_all, counters)
+            self.graph_stats["captured"] += 1
+            return x_out, blocks_all, counters
+        g, x_cap, blocks_all, counters = entry
+        with torch.cuda.stream(s):
+            x_cap.f32.copy_(x_in.f32)
+            x_cap.bf16.copy_(x_in.bf16)
+            g.replay()
+        self.graph_stats["replayed"] += 1
+        return x_cap, blocks_all, counters
 
     def _classify(self) -> None:
         cfg = self.config
@@ -537,10 +613,19 @@ class Session:
         final_kv = []
         step_counters: list[StepCounters] = []
         x = None
+        graphed = False
         for t in range(cfg.denoise_steps):
             x = self.model.frame_input(ar_step, t)
             final = t == cfg.denoise_steps - 1
             ratios = sorted(self._probe_requests.get((ar_step, t), ()))
+            if self._graphable(ratios):
+                x, blocks_all, counters = self._graph_iteration(x, ar_step, t)
+                graphed = True
+                if final:  # the views are the pending ring slots; the frame id is this step's
+                    final_kv = [[FrameBlock(ar_step, b.keys, b.values) for b in row] for row in blocks_all]
+                step_counters.append(counters)
+                continue
+            graphed = False
             probes: dict[float, list[ProbeRequest]] = {r: [] for r in ratios}
             counters = StepCounters()
             for layer in range(cfg.num_layers):
@@ -575,7 +660,8 @@ class Session:
         if segs:
             launch_segments(segs, s)
         self._after_step(ar_step)
-        self._frames.append(getattr(x, "f32", x))
+        frame = getattr(x, "f32", x)
+        self._frames.append(frame.clone() if graphed else frame)  # graph buffers are reused by the next replay
         self._step_counters.append((ar_step, step_counters))
         self._kernel_calls_last = list(step_counters[-1].kernel_calls)
         self._phys_last = [lc.physical_launches for lc in step_counters[-1].layers]
@@ -659,7 +745,7 @@ class Session:
             kernel_calls_steady=self._kernel_calls_last,
             total_key_token_macs=sum(s["key_token_macs"] for s in steps),
             total_wall_time_ns=sum(s["wall_time_ns"] for s in steps),
-            output_digest=_digest(self._frames),
+            frames=list(self._frames),
             physical_launches_steady=self._phys_last,
         )
 

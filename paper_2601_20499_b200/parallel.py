@@ -101,6 +101,9 @@ class HeadParallelSession(Session):
             d8 = ((config.head_dim + 7) // 8) * 8
             self.fused = FusedHeadGather(config.num_heads * config.HW, d8, group, self.device)
 
+    def _graphable(self, ratios) -> bool:
+        return False  # per-layer collectives (NCCL or the symmetric-memory barrier) stay eager
+
     def _output_target(self, layer: int):
         if self.fused is None:
             return None
