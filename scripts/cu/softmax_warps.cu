@@ -27,13 +27,25 @@ __global__ void __launch_bounds__(256, 1) k(unsigned* out, const float* src, int
       for (int i = 0; i < 16; ++i) {
         const int c = q * 32 + 2 * i;
         const float2 x = fma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
-        float2 e;
-        if (((c / 2) * EMU) % 8 < EMU)
-          e = exp2_poly2(x, eu);
-        else
-          e = make_float2(ex2(x.x), ex2(x.y));
-        sum2 = add2(sum2, e);
-        pk[i] = pack_bf16x2(e.x, e.y);
+        if constexpr (EMU == -2 || EMU == -3 || EMU == -4) {  // ablations: -2 no F2FP, -3 no FADD2, -4 neither
+          float2 e = make_float2(ex2(x.x), ex2(x.y));
+          if (EMU != -3 && EMU != -4) ;
+          if (EMU == -2) sum2 = add2(sum2, e);
+          pk[i] = (EMU == -3) ? pack_bf16x2(e.x, e.y) : (__float_as_uint(e.x) ^ __float_as_uint(e.y));
+        } else if constexpr (EMU < 0) {  // packed bf16x2 MUFU: P directly, f32 row sum from the bf16 halves
+          uint32_t xb = pack_bf16x2(x.x, x.y), pb;
+          asm("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(pb) : "r"(xb));
+          pk[i] = pb;
+          sum2 = add2(sum2, make_float2(__uint_as_float(pb << 16), __uint_as_float(pb & 0xffff0000u)));
+        } else {
+          float2 e;
+          if (((c / 2) * EMU) % 8 < EMU)
+            e = exp2_poly2(x, eu);
+          else
+            e = make_float2(ex2(x.x), ex2(x.y));
+          sum2 = add2(sum2, e);
+          pk[i] = pack_bf16x2(e.x, e.y);
+        }
       }
 #pragma unroll
       for (int i = 0; i < 16; ++i) acc += pk[i];
@@ -57,7 +69,7 @@ void run(unsigned* d, const float* src, long long* cyc, int sms) {
     long long h;
     cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
     const double per_tile = double(h) / iters;  // cycles per 128-col row tile per warp
-    printf("emu %d/8 max %d warps/SMSP %d: %.0f cycles per row-tile per warp (%.1f exps/clk/SM)\n", EMU, MAX,
+    printf("emu %d/8 (-1: bf16x2 ex2) max %d warps/SMSP %d: %.0f cycles per row-tile per warp (%.1f exps/clk/SM)\n", EMU, MAX,
            threads / 128, per_tile, threads / 32 * 32 * 128 / per_tile);
   }
 }
@@ -76,6 +88,9 @@ int main() {
   }
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  run<-2, false>(d, src, cyc, sms);
+  run<-3, false>(d, src, cyc, sms);
+  run<-4, false>(d, src, cyc, sms);
   run<0, false>(d, src, cyc, sms);
   run<0, true>(d, src, cyc, sms);
   run<1, true>(d, src, cyc, sms);
