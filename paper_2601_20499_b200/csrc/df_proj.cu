@@ -228,8 +228,12 @@ __global__ void __launch_bounds__(kPThreads, 1) df_proj_kernel(const __grid_cons
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // Warp-wide loop, elected lane issues; descriptors are a precomputed base
+    // plus compile-time offsets (as the FMHA issuer).
+    {
       constexpr uint32_t idesc = idesc_bf16(kPBM, BN, false);
+      const uint64_t d0 = sdesc_sw128(smem_u32(smem), 16, 1024);
+      constexpr uint64_t kStageDesc = C::kStageBytes >> 4, kBDesc = C::kABytes >> 4;
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -241,19 +245,17 @@ __global__ void __launch_bounds__(kPThreads, 1) df_proj_kernel(const __grid_cons
         for (int kb = 0; kb < p.kblocks; ++kb) {
           mbar_wait(full + stage, phase);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
-          const uint32_t sb = sa + C::kABytes;
+          const uint64_t da = d0 + stage * kStageDesc;
 #pragma unroll
           for (int k = 0; k < kPBK / 16; ++k)
-            umma_ss(d, sdesc_sw128(sa + k * 32, 16, 1024), sdesc_sw128(sb + k * 32, 16, 1024), idesc,
-                    (kb | k) != 0);
-          umma_commit(empty + stage);
+            umma_ss_elect(d, da + ((k * 32) >> 4), da + kBDesc + ((k * 32) >> 4), idesc, (kb | k) != 0);
+          umma_commit_elect(empty + stage);
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        umma_commit(acc_full + acc);
+        umma_commit_elect(acc_full + acc);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
