@@ -306,6 +306,185 @@ __global__ void __launch_bounds__(kPThreads, 1) df_proj_kernel(const __grid_cons
   }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2, M = 256 per MMA).  A cluster of two CTAs on
+// one TPC computes a 256 x BN tile: each CTA stages its 128 rows of A and half
+// of the BN rows of B, so per SM the B reads and B TMA writes halve -- the
+// 1-CTA kernel moves ~192 B/clk through shared memory per 128-cycle UMMA
+// against a 128 B/clk port, this one ~128.  The leader's elected lane issues
+// for both SMs; each CTA's epilogue warps drain its own 128 accumulator rows
+// and release the accumulator on the leader's barrier.
+template <int BN, int kEpi>
+struct PairCfg {
+  static constexpr int kABytes = kPBM * kPBK * 2;
+  static constexpr int kBBytes = (BN / 2) * kPBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStgWarp = 32 * StageRow<kEpi>::kBytes;
+  static constexpr int kBudget = 232448 - 1024 - 256;
+  static constexpr int kFit = (kBudget - kEpiWarps * kStgWarp) / kStageBytes;
+  static constexpr int kStages = kFit > 8 ? 8 : kFit;
+  static constexpr int kStgOff = kStages * kStageBytes;
+  static constexpr int kBarOff = kStgOff + kEpiWarps * kStgWarp;
+  static constexpr int kSmem = kBarOff + (2 * kStages + 4) * 8 + 16 + 1024;
+  static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
+  static_assert(kStages >= 3, "pipeline too shallow");
+  static_assert(kSmem <= 232448, "shared memory");
+};
+
+template <int BN, int kEpi>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
+    df_proj_pair_kernel(const __grid_constant__ ProjParams p) {
+  using C = PairCfg<BN, kEpi>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kBarOff);  // leader: A + B of both CTAs landed
+  uint64_t* empty = full + C::kStages;                               // both: the stage's MMAs are done
+  uint64_t* acc_full = empty + C::kStages;                           // [2] both
+  uint64_t* acc_empty = acc_full + 2;                                // [2] leader: both epilogues drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const int cid = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(acc_full + a, 1);
+      mbar_init(acc_empty + a, 2 * kEpiWarps);  // one arrive per epilogue warp of either CTA
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      prefetch_tmap(&p.amap);
+      prefetch_tmap(&p.bmap);
+      const uint64_t pol = policy_evict_last();  // W and x tiles are re-read by other clusters
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cid; tile < p.tiles; tile += nclusters) {
+        const int mb = tile % p.m_tiles;
+        const int nb = tile / p.m_tiles;
+        for (int kb = 0; kb < p.kblocks; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          if (crank == 0) mbar_expect_tx(full + stage, 2 * C::kStageBytes);
+          const uint32_t lbar = mapa_shared(smem_u32(full + stage), 0);
+          const int kk = kb * kPBK;
+          const int chunk = kk / p.a_cols;
+          uint8_t* sa = smem + stage * C::kStageBytes;
+          tma_load_2d_pair(sa, &p.amap, lbar, kk - chunk * p.a_cols,
+                           mb * 2 * kPBM + static_cast<int>(crank) * kPBM + chunk * p.a_chunk_rows, pol);
+          tma_load_2d_pair(sa + C::kABytes, &p.bmap, lbar, kk, nb * BN + static_cast<int>(crank) * (BN / 2), pol);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader, warp-wide, elected lane)
+    if (crank == 0) {
+      constexpr uint32_t idesc = idesc_bf16(2 * kPBM, BN, false);
+      const uint64_t d0 = sdesc_sw128(smem_u32(smem), 16, 1024);
+      constexpr uint64_t kStageDesc = C::kStageBytes >> 4, kBDesc = C::kABytes >> 4;
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cid; tile < p.tiles; tile += nclusters) {
+        mbar_wait_cluster(acc_empty + acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < p.kblocks; ++kb) {
+          mbar_wait_cluster(full + stage, phase);
+          tc_fence_after();
+          const uint64_t da = d0 + stage * kStageDesc;
+#pragma unroll
+          for (int k = 0; k < kPBK / 16; ++k)
+            umma_ss_pair_elect(d, da + ((k * 32) >> 4), da + kBDesc + ((k * 32) >> 4), idesc, (kb | k) != 0);
+          umma_commit_pair_elect(empty + stage);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair_elect(acc_full + acc);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (both CTAs, own 128 rows)
+    const int quad = warp & 3;
+    constexpr int kPer = BN / 64;
+    const int c0 = ((warp - 2) >> 2) * kPer;
+    uint8_t* stg = smem + C::kStgOff + (warp - 2) * C::kStgWarp;
+    const uint32_t leader_acc_empty = mapa_shared(smem_u32(acc_empty), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = cid; tile < p.tiles; tile += nclusters) {
+      const int mb = tile % p.m_tiles;
+      const int nb = tile / p.m_tiles;
+      mbar_wait_cluster(acc_full + acc, acc_phase);
+      tc_fence_after();
+      const int row0 = mb * 2 * kPBM + static_cast<int>(crank) * kPBM + quad * 32;
+      const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(quad * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < kPer; ++c) {
+        uint32_t r[32];
+        tmem_ld32(taddr + (c0 + c) * 32, r);
+        tmem_wait_ld();
+        epilogue_chunk<kEpi>(p, stg, lane, row0, nb * BN + (c0 + c) * 32, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_acc_empty + acc * 8);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer's smem and TMEM stay live until the leader's MMAs are done
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, C::kTmemCols);
+  }
+}
+
+template <int BN, int kEpi>
+int launch_proj_pair(const ProjParams& p, int grid, cudaStream_t stream) {
+  auto kern = df_proj_pair_kernel<BN, kEpi>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<BN, kEpi>::kSmem);
+    if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(df_proj_pair_kernel)", e);
+    configured = true;
+  }
+  kern<<<grid, kPThreads, PairCfg<BN, kEpi>::kSmem, stream>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error("df_proj_pair_kernel launch", e);
+  return DF_OK;
+}
+
 template <int BN, int kEpi>
 int launch_proj(const ProjParams& p, int grid, cudaStream_t stream) {
   auto kern = df_proj_kernel<BN, kEpi>;
@@ -321,37 +500,71 @@ int launch_proj(const ProjParams& p, int grid, cudaStream_t stream) {
   return DF_OK;
 }
 
-// Tile width N: smallest modelled time over whole waves of the persistent
-// grid.  Per-tile cost ~ N / eff(N): with both operands in shared memory an
-// N=128 tile is bound by shared-memory bandwidth (measured 0.66 of the N=256
-// rate on B200), N=192 at 0.86.
-int pick_bn(int64_t m, int64_t n) {
-  if (const char* env = std::getenv("DF_PROJ_BN")) {
-    const int v = std::atoi(env);
-    if (v == 128 || v == 192 || v == 256) return v;
-  }
-  const int64_t sms = sm_count_cached();
-  const int64_t mt = (m + kPBM - 1) / kPBM;
-  double best = 1e300;
-  int bn = 256;
-  for (int cand : {256, 192, 128}) {
-    const double eff = cand == 256 ? 1.0 : (cand == 192 ? 0.86 : 0.66);
-    const int64_t tiles = mt * ((n + cand - 1) / cand);
-    const int64_t waves = (tiles + sms - 1) / sms;
-    const double cost = double(waves) * cand / eff;
-    if (cost < best * 0.999) {
-      best = cost;
-      bn = cand;
-    }
-  }
-  return bn;
-}
-
 template <int kEpi>
-int launch_bn(int bn, const ProjParams& p, int grid, cudaStream_t s) {
+int launch_bn(int bn, bool pair, const ProjParams& p, int grid, cudaStream_t s) {
+  if (pair) {
+    if (bn == 256) return launch_proj_pair<256, kEpi>(p, grid, s);
+    if (bn == 192) return launch_proj_pair<192, kEpi>(p, grid, s);
+    return launch_proj_pair<128, kEpi>(p, grid, s);
+  }
   if (bn == 256) return launch_proj<256, kEpi>(p, grid, s);
   if (bn == 192) return launch_proj<192, kEpi>(p, grid, s);
   return launch_proj<128, kEpi>(p, grid, s);
+}
+
+// CTA-pair GEMM unless DF_PROJ_PAIR=0 (dev A/B).
+bool use_pair_gemm() {
+  static const bool on = [] {
+    const char* env = std::getenv("DF_PROJ_PAIR");
+    return !(env && env[0] == '0');
+  }();
+  return on;
+}
+
+// Tiling of an (m x n) projection: tile width, 1-CTA or pair, tiles and grid.
+struct Tiling {
+  int bn;
+  bool pair;
+  int32_t m_tiles, tiles;
+  int grid;
+};
+
+Tiling pick_tiling(int64_t m, int64_t n) {
+  // Smallest modelled time over whole waves of the persistent grid: cost = waves x N / eff, with eff the
+  // measured per-SM rate of a 128 x N slice (1-CTA: shared-memory bound below N = 256, 0.66 at 128,
+  // 0.86 at 192; the pair halves B traffic: 1.07 at N = 256 against the 1-CTA N = 256 rate).  Wan:
+  // QKV takes the pair at N = 256 (342 pair tiles), the out-projection the 1-CTA kernel at N = 192
+  // (296 tiles = 2 waves; the pair's 114 tiles waste half a wave).
+  int forced = 0;
+  if (const char* env = std::getenv("DF_PROJ_BN")) {
+    const int v = std::atoi(env);
+    forced = (v == 128 || v == 192 || v == 256) ? v : 0;
+  }
+  const int64_t sms = sm_count_cached();
+  Tiling best{256, false, 0, 0, 0};
+  double best_cost = 1e300;
+  for (int pair = use_pair_gemm() ? 1 : 0; pair >= 0; --pair) {
+    const int64_t rows = pair ? 2 * kPBM : kPBM;
+    const int64_t units = pair ? sms / 2 : sms;
+    for (int cand : {256, 192, 128}) {
+      if (forced && cand != forced) continue;
+      const double eff = pair ? (cand == 256 ? 1.07 : (cand == 192 ? 1.0 : 0.9))
+                              : (cand == 256 ? 1.0 : (cand == 192 ? 0.86 : 0.66));
+      const int64_t tiles = ((m + rows - 1) / rows) * ((n + cand - 1) / cand);
+      const int64_t waves = (tiles + units - 1) / units;
+      const double cost = double(waves) * cand / eff;
+      if (cost < best_cost * 0.999) {
+        best_cost = cost;
+        best.bn = cand;
+        best.pair = pair != 0;
+        best.m_tiles = static_cast<int32_t>((m + rows - 1) / rows);
+        best.tiles = static_cast<int32_t>(tiles);
+        const int64_t u = tiles < units ? tiles : units;
+        best.grid = static_cast<int>(pair ? 2 * u : u);
+      }
+    }
+  }
+  return best;
 }
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; }
@@ -396,16 +609,15 @@ extern "C" int df_qkv_project(const df_qkv_args* a, void* stream) {
   p.qkv_cols = cols;
   p.q_out = static_cast<__nv_bfloat16*>(a->q_out);
   p.kv_ld = a->kv_ld;
-  const int bn = pick_bn(p.m, p.n);
+  const Tiling t = pick_tiling(p.m, p.n);
   rc = encode_bf16_2d(&p.amap, a->x, a->hw, a->in_dim, a->in_dim, kPBM);
   if (rc != DF_OK) return rc;
-  rc = encode_bf16_2d(&p.bmap, a->w_qkv, int64_t(p.n), a->in_dim, a->in_dim, bn);
+  rc = encode_bf16_2d(&p.bmap, a->w_qkv, int64_t(p.n), a->in_dim, a->in_dim, t.pair ? t.bn / 2 : t.bn);
   if (rc != DF_OK) return rc;
-  p.m_tiles = (p.m + kPBM - 1) / kPBM;
-  p.tiles = p.m_tiles * ((p.n + bn - 1) / bn);
-  const int grid = p.tiles < sm_count_cached() ? p.tiles : sm_count_cached();
+  p.m_tiles = t.m_tiles;
+  p.tiles = t.tiles;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  return launch_bn<kEpiQKV>(bn, p, grid, s);
+  return launch_bn<kEpiQKV>(t.bn, t.pair, p, t.grid, s);
 }
 
 extern "C" int df_out_project(const df_oproj_args* a, void* stream) {
@@ -429,14 +641,13 @@ extern "C" int df_out_project(const df_oproj_args* a, void* stream) {
   p.out_ld = a->out_dim;
   p.x = a->x;
   p.x_bf16 = static_cast<__nv_bfloat16*>(a->x_bf16);
-  const int bn = pick_bn(p.m, p.n);
+  const Tiling t = pick_tiling(p.m, p.n);
   rc = encode_bf16_2d(&p.amap, a->o, int64_t(a->num_heads) * a->hw, a->head_dim, a->head_dim, kPBM);
   if (rc != DF_OK) return rc;
-  rc = encode_bf16_2d(&p.bmap, a->w_o, a->out_dim, kdim, kdim, bn);
+  rc = encode_bf16_2d(&p.bmap, a->w_o, a->out_dim, kdim, kdim, t.pair ? t.bn / 2 : t.bn);
   if (rc != DF_OK) return rc;
-  p.m_tiles = (p.m + kPBM - 1) / kPBM;
-  p.tiles = p.m_tiles * ((p.n + bn - 1) / bn);
-  const int grid = p.tiles < sm_count_cached() ? p.tiles : sm_count_cached();
+  p.m_tiles = t.m_tiles;
+  p.tiles = t.tiles;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  return launch_bn<kEpiOut>(bn, p, grid, s);
+  return launch_bn<kEpiOut>(t.bn, t.pair, p, t.grid, s);
 }
