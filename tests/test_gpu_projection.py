@@ -187,3 +187,53 @@ def test_session_cuda_graphs_equal_eager():
     assert s.graph_stats["captured"] < cfg.ar_steps  # the warm ring cycles through its slots
     # frames are distinct tensors (the graph's residual buffers are reused)
     assert len({f.data_ptr() for f in b}) == len(b)
+
+
+_PAIR_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2601_20499_b200 import kernels as K
+torch.manual_seed(0)
+dev = torch.device("cuda")
+for (hw, H, d) in ((4680, 12, 128), (300, 4, 64), (1000, 3, 128)):
+    D = H * d
+    x = torch.randn(hw, D, device=dev).to(torch.bfloat16)
+    w = (torch.randn(3 * D, D, device=dev) / D ** 0.5).to(torch.bfloat16)
+    q = torch.empty(H, hw, d, dtype=torch.bfloat16, device=dev)
+    k = torch.empty_like(q)
+    v = torch.empty_like(q)
+    K.prepare_qkv_projection(x, w, q, list(k), list(v), d).launch()
+    o = torch.randn(H, hw, d, device=dev).to(torch.bfloat16)
+    wo = (torch.randn(D, D, device=dev) / D ** 0.5).to(torch.bfloat16)
+    xf = torch.randn(hw, D, device=dev)
+    xb = torch.empty(hw, D, dtype=torch.bfloat16, device=dev)
+    K.prepare_out_projection(o, wo, xf, xb, d).launch()
+    torch.cuda.synchronize()
+    ref_q = (x.float() @ w.float().T)[:, :D].reshape(hw, H, d).transpose(0, 1)
+    err = ((q.float() - ref_q).abs().max() / ref_q.abs().max()).item()
+    assert err < 1e-2, err
+    torch.save({"q": q.cpu(), "k": k.cpu(), "v": v.cpu(), "xf": xf.cpu(), "xb": xb.cpu()}, f"{sys.argv[2]}_{hw}.pt")
+"""
+
+
+@pytest.mark.parametrize("bn", ["", "128", "256"])
+def test_pair_and_single_cta_gemms_bitwise_equal(tmp_path, bn):
+    """The CTA-pair projection GEMM (cta_group::2) and the 1-CTA GEMM produce bitwise identical Q/K/V and
+    residual updates (same K order per output element), on the Wan shape and ragged ones, with the
+    tiling picker free or forced to N = 128 / 256 (subprocesses: DF_PROJ_PAIR / DF_PROJ_BN are read once)."""
+    import subprocess
+    import sys as _sys
+
+    script = tmp_path / "pair.py"
+    script.write_text(_PAIR_SCRIPT)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for pair in ("0", "1"):
+        env = dict(os.environ, DF_PROJ_PAIR=pair)
+        if bn:
+            env["DF_PROJ_BN"] = bn
+        subprocess.run([_sys.executable, str(script), root, str(tmp_path / f"p{pair}")], check=True, env=env)
+    for hw in (4680, 300, 1000):
+        a = torch.load(tmp_path / f"p0_{hw}.pt")
+        b = torch.load(tmp_path / f"p1_{hw}.pt")
+        for key in a:
+            assert torch.equal(a[key], b[key]), (hw, key)
