@@ -14,13 +14,15 @@
 // Persistent kernel, one CTA per SM, 320 threads:
 //   warp 0      TMA producer: [128 x 64] A box + [BN x 64] B box per stage
 //               (SWIZZLE_128B), kStages-deep ring
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer,
+//   warp 1      TMEM allocator + tcgen05.mma issuer (elected lane),
 //               accumulators double-buffered in TMEM (2 x BN fp32 columns)
 //   warps 2-9   epilogue (two per TMEM lane quadrant, half the columns
 //               each): tcgen05.ld 32 columns, staged through shared memory,
 //               row-contiguous fused loads/stores, overlapping the next
 //               tile's main loop
 // Tiles are walked m-fastest so consecutive CTAs share the same W tile in L2.
+// df_proj_pair_kernel is the CTA-pair (cta_group::2, M = 256) form of the same
+// GEMM; pick_tiling chooses the variant and N per shape by whole-wave cost.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
