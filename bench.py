@@ -403,7 +403,42 @@ def kernel_configs(df, dev, bf16_peak):
         "packed_6d3s3n_logit_std3": one(PACKED_CTX, HW, 3.0),
         "hires_c4_packed_6d3s3n": one([2 * hr] * 9 + [6 * hr] * 3, hr),
         "hires_c4_all_context": one([7 * hr] * 12, hr),
+        # C5 context extension: the budget freed by sink/dummy heads goes to the neighbor heads
+        # (kv_cache.py:143-158, 6d/3s/3n: 21 frames per neighbor head), FLOPs equal to all-context
+        "context_extension_c5": one([2 * HW] * 9 + [22 * HW] * 3, HW),
     }
+    # C5: B independent streams' packed layers in ONE launch (batched_step; 4 arenas, 48 heads)
+    B = 4
+    arenas = []
+    for _ in range(B):
+        a = K.KVArena(sum(K.KVArena.region_rows(c) for c in PACKED_CTX), D, dev)
+        a.k.normal_()
+        a.v.normal_()
+        arenas.append(a)
+    qb = torch.randn(B * H * HW, D, device=dev).to(torch.bfloat16)
+    ob = torch.empty(B * H * HW, D, device=dev, dtype=torch.bfloat16)
+    wb = [K.HeadWork(a, a.allocate(c), c, b * H + h, b * H + h) for b, a in enumerate(arenas)
+          for h, c in enumerate(PACKED_CTX)]
+    lb = K.prepare_attention(qb, ob, wb, HW, 1 / math.sqrt(D))
+    for _ in range(3):
+        for l in lb:
+            l.launch(None)
+    ts = []
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for l in lb:
+            l.launch(None)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    us = sorted(ts)[len(ts) // 2] * 1e3
+    tf = B * 4 * D * HW * sum(PACKED_CTX) / (us * 1e-6) / 1e12
+    res["streams4_batched_c5"] = {"us_per_layer_all_streams": us, "us_per_layer_per_stream": us / B, "tflops": tf,
+                                  "frac": tf / bf16_peak, "launches": len(lb),
+                                  "note": "4 independent packed Wan layers (4 arenas, 48 heads) in one FMHA launch"}
+    del arenas, qb, ob
+    torch.cuda.empty_cache()
     res["hires_c4_speedup_packed_vs_all_context"] = (res["hires_c4_all_context"]["us_per_layer"]
                                                      / res["hires_c4_packed_6d3s3n"]["us_per_layer"])
     res["timing"] = "single launch, CUDA events, median of 10 (burst clocks)"

@@ -268,6 +268,120 @@ def packed_step(q_heads, caches, current_blocks, classes: list[HeadClass], confi
     return _dispatch(q_heads, caches, current_blocks, config.head_dim, [ds, nb], probe, stream, timed, target)
 
 
+@dataclass
+class StepRequest:
+    """One session's layer for ``batched_step``: the arguments of baseline_step / hma_step / packed_step."""
+
+    mode: str
+    q_heads: object
+    caches: list
+    current_blocks: list
+    classes: list | None = None
+
+
+def _request_groups(r: StepRequest, config: SessionConfig) -> list[list[int]]:
+    """The logical calls of one request, with the checks of the matching step function."""
+    if r.mode == "baseline":
+        for c in r.caches:
+            if c.policy.kind != "baseline_window":
+                raise ConfigError(f"baseline_step got a {c.policy.kind} cache")
+        return [list(range(len(r.caches)))]
+    if r.mode not in ("hma", "packed"):
+        raise ConfigError(f"unknown mode {r.mode!r}, expected one of {MODES}")
+    classes = list(r.classes or [])
+    if len(classes) != len(r.caches):
+        raise AssignmentError(f"{len(classes)} classes for {len(r.caches)} heads in this layer")
+    if r.mode == "hma":
+        return _class_groups(classes)
+    if not config.packing_enabled:
+        raise ConfigError("packed_step requires packing_enabled")
+    return [[h for h, c in enumerate(classes) if c is not HeadClass.NEIGHBOR],
+            [h for h, c in enumerate(classes) if c is HeadClass.NEIGHBOR]]
+
+
+def batched_step(requests: Sequence[StepRequest], config: SessionConfig, *, stream=None, timed: bool = True):
+    """Several independent sessions' layers (SURVEY 8(e) / BASELINE configs[4]: a batch of video streams
+    on one GPU) in ONE ragged FMHA launch (more launches only past DF_MAX_HEADS heads or DF_MAX_ARENAS
+    arenas).  Each request keeps its own logical calls, MAC counters and errors; the batch fills the
+    SMs' last wave that a single stream's layer leaves partly idle.  Returns [(outputs, LayerCounters)]
+    in request order; the outputs are views of one batched buffer.
+    """
+    if not requests:
+        raise ShapeError("no requests")
+    groups = [_request_groups(r, config) for r in requests]
+    d = config.head_dim
+    hw = requests[0].current_blocks[0].tokens if requests[0].current_blocks else config.HW
+    device = None
+    for r in requests:
+        if len(r.current_blocks) != len(r.caches) or not r.caches:
+            raise ShapeError(f"{len(r.current_blocks)} current blocks for {len(r.caches)} caches")
+        for c, b in zip(r.caches, r.current_blocks):
+            if b.tokens != hw:
+                raise ShapeError("current blocks of one batch must share HW")
+            c.check_current(b.frame_id)
+        if device is None and isinstance(r.q_heads, torch.Tensor) and r.q_heads.is_cuda:
+            device = r.q_heads.device
+    if device is None:
+        device = requests[0].caches[0].storage.arena.device
+    width = requests[0].caches[0].storage.arena.width
+    d8 = ((d + 7) // 8) * 8
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    ctx = torch.cuda.stream(stream) if stream is not None else None
+    if ctx is not None:
+        ctx.__enter__()
+    try:
+        counters, segs, work, qs = [], [], [], []
+        base = 0
+        for r, g in zip(requests, groups):
+            n_tok = [c.context_tokens(hw) for c in r.caches]
+            calls = macs = 0
+            for grp in g:
+                if not grp:
+                    continue
+                lens = {n_tok[h] for h in grp}
+                if len(lens) != 1:
+                    raise PackingError(f"context lengths {sorted(lens)} differ within one batch")
+                calls += 1
+                macs += len(grp) * hw * n_tok[grp[0]] * d
+            counters.append(LayerCounters(kernel_calls=calls, key_token_macs=macs, physical_launches=0))
+            for c, b in zip(r.caches, r.current_blocks):
+                segs += c.stage_segments(b, device)
+            qs.append(_q_rows(r.q_heads, len(r.caches), hw, d, width, device))
+            work += [K.HeadWork(c.storage.arena, c.storage.base_row, n_tok[h], base + h, base + h)
+                     for h, c in enumerate(r.caches)]
+            base += len(r.caches)
+        q2 = qs[0] if len(qs) == 1 else torch.cat(qs, 0)
+        out = torch.empty(base * hw, d8, dtype=torch.bfloat16, device=device)
+        copies = K.prepare_copies([sg[:6] for sg in segs])
+        attn = K.prepare_attention(q2, out, work, hw, 1.0 / math.sqrt(d), None, None, s)
+        if timed:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record(s)
+        for launch in copies:
+            launch.launch(s)
+        if timed:
+            ev[1].record(s)
+        for launch in attn:
+            launch.launch(s)
+        if timed:
+            ev[2].record(s)
+        del segs
+    finally:
+        if ctx is not None:
+            ctx.__exit__(None, None, None)
+    o = out.view(base, hw, d8)
+    if d8 != d:
+        o = o[..., :d]
+    res, h0 = [], 0
+    for r, lc in zip(requests, counters):
+        lc.physical_launches = len(copies) + len(attn)
+        if timed:
+            lc._events = tuple(ev)
+        res.append((o[h0:h0 + len(r.caches)], lc))
+        h0 += len(r.caches)
+    return res
+
+
 def expected_step_macs(config: SessionConfig, mode: str, history_frames: int,
                        assignment: HeadAssignment | None = None) -> int:
     """Closed-form key-token MACs of one denoise iteration (engine.py:198-237)."""

@@ -213,6 +213,49 @@ def test_wan_layer_full_size_properties():
         assert (o_p[h].float() - ref).abs().max() / ref.abs().max() <= TOL
 
 
+def test_batched_step_streams_in_one_launch():
+    """batched_step (BASELINE configs[4]: several streams on one GPU): a packed, an hma and a baseline
+    request from three sessions (three arenas) in one FMHA launch; every request's outputs match its own
+    step call (fp32-rounding level: the split plan of the batch differs) and fp32 torch, its counters
+    and errors are those of the single-request step, and bad requests raise the reference exceptions."""
+    H, HW, d, W = 4, 600, 128, 4
+    cfg = df.SessionConfig(num_layers=1, num_heads=H, head_dim=d, HW=HW, window_len=W, ar_steps=7, dummy_count=2)
+    g = torch.Generator(device=DEV).manual_seed(5)
+    rnd = lambda *sh: torch.randn(*sh, device=DEV, generator=g).to(torch.bfloat16)
+
+    def session():
+        caches = []
+        for h in range(H):
+            c = df.HeadKVCache(df.baseline_policy(cfg))
+            for f in range(5):
+                c.append_and_evict(df.FrameBlock(f, rnd(HW, d), rnd(HW, d)))
+            caches.append(c)
+        return caches, rnd(H, HW, d), [df.FrameBlock(5, rnd(HW, d), rnd(HW, d)) for _ in range(H)]
+
+    classes = [df.HeadClass.DUMMY, df.HeadClass.SINK, df.HeadClass.NEIGHBOR, df.HeadClass.DUMMY]
+    (c0, q0, b0), (c1, q1, b1), (c2, q2, b2) = session(), session(), session()
+    p0 = df.rebuild_caches(c0, [df.derive_policy(c, cfg) for c in classes])
+    p1 = df.rebuild_caches(c1, [df.derive_policy(c, cfg) for c in classes])
+    c2 = df.rebuild_caches(c2, [df.baseline_policy(cfg)] * H)  # one arena per session: 3 arenas, 1 launch
+    reqs = [df.StepRequest("packed", q0, p0, b0, classes), df.StepRequest("hma", q1, p1, b1, classes),
+            df.StepRequest("baseline", q2, c2, b2)]
+    got = df.batched_step(reqs, cfg)
+    singles = [df.packed_step(q0, p0, b0, classes, cfg), df.hma_step(q1, p1, b1, classes, cfg),
+               df.baseline_step(q2, c2, b2, cfg)]
+    for (o, lc), (o1, lc1), r in zip(got, singles, reqs):
+        assert (lc.kernel_calls, lc.key_token_macs) == (lc1.kernel_calls, lc1.key_token_macs)
+        assert lc.physical_launches == 2  # one staging-copy launch + ONE attention launch for all 12 heads
+        assert (o.float() - o1.float()).abs().max() / o1.float().abs().max() <= 4e-3
+        for h in range(H):
+            k, v, _ = r.caches[h].gather_context(r.current_blocks[h])
+            ref = torch.softmax((r.q_heads[h].float() @ k.float().T) / math.sqrt(d), -1) @ v.float()
+            assert (o[h].float() - ref).abs().max() / ref.abs().max() <= TOL
+    with pytest.raises(df.AssignmentError):
+        df.batched_step([df.StepRequest("packed", q0, p0, b0, classes[:3])], cfg)
+    with pytest.raises(df.ConfigError):
+        df.batched_step([df.StepRequest("baseline", q0, p0, b0)], cfg)
+
+
 def test_head_parallel_session_world1_matches_session():
     """HeadParallelSession wiring on the NCCL backend (one rank on this GPU):
     identical classes, scores and outputs to the plain Session."""
