@@ -108,8 +108,11 @@ typedef struct df_attn_args {
   const uint8_t* region_of_slot;  /* probe, device [num_heads][max_slots]; 0 sink 1 neighbor 2 current */
   const uint8_t* row_sampled;     /* probe, device [hw] (profiler.py:132-144) */
   float* probe_rows;              /* probe, device [num_heads][hw][3] region masses per sampled row */
-  /* Split-KV workspace (device, caller-owned, zero-filled once; the kernel
-   * leaves its counters at zero).  NULL or too small => no kv splitting. */
+  /* Split-KV workspace (device, caller-owned, zero-filled once).  Layout:
+   * fp32 partials from the start, combine counters in the LAST 64 KB; every
+   * launch leaves its counters at zero, so pass the same buffer with the same
+   * workspace_bytes every time (the counters' position follows the size).
+   * NULL or smaller than df_attn_workspace_bytes => no kv splitting. */
   void* workspace;
   int64_t workspace_bytes;
   /* Fused head-output all-gather (head-parallel sessions, SURVEY 8(e) / 8(f)

@@ -1195,7 +1195,15 @@ void order_heads(const df_attn_args* a, const uint8_t* ns, int* order) {
   });
 }
 
-int64_t workspace_need(const df_attn_args* a, const uint8_t* ns, bool pair) {
+// Split-KV workspace layout: [fp32 partials (O, then m/l/region masses) | ... | combine counters].
+// The counters live in a FIXED region at the END of the caller's workspace
+// (kCntBytes), so a later launch with more split groups never reads an earlier
+// launch's partials as counters: the region is zero when allocated and every
+// launch leaves its counters at zero, whatever the partial sizes in between.
+constexpr int64_t kCntBytes = 64 * 1024;  // 16384 counters: groups x ranks
+constexpr int64_t kMaxCounters = kCntBytes / 4;
+
+int64_t split_groups(const df_attn_args* a, const uint8_t* ns, bool pair, int64_t* slots_out) {
   const int R = item_rows(pair);
   const int nq = (a->hw + R - 1) / R;
   int64_t groups = 0, slots = 0;
@@ -1204,10 +1212,16 @@ int64_t workspace_need(const df_attn_args* a, const uint8_t* ns, bool pair) {
       groups += nq;
       slots += int64_t(nq) * ns[h];
     }
-  if (!groups) return 0;
+  if (slots_out) *slots_out = slots;
+  return groups;
+}
+
+int64_t workspace_need(const df_attn_args* a, const uint8_t* ns, bool pair) {
+  int64_t slots = 0;
+  if (!split_groups(a, ns, pair, &slots)) return 0;
   const int64_t ranks = pair ? 2 : 1;
-  const int64_t cnt_bytes = ((groups * ranks * 4 + 255) / 256) * 256;
-  return cnt_bytes + slots * ranks * 256 * (int64_t(a->head_dim) + 8) * 4;
+  const int64_t part_bytes = ((slots * ranks * 256 * (int64_t(a->head_dim) + 8) * 4 + 255) / 256) * 256;
+  return part_bytes + kCntBytes;
 }
 
 Plan make_plan(const df_attn_args* a, bool allow_split, bool pair) {
@@ -1226,6 +1240,7 @@ Plan make_plan(const df_attn_args* a, bool allow_split, bool pair) {
         const int tiles = (a->heads[h].n_tok + 127) / 128;
         c.ns[h] = static_cast<uint8_t>(std::min(kMaxSplit, std::max(1, (tiles + cap - 1) / cap)));
       }
+      if (split_groups(a, c.ns, pair, nullptr) * (pair ? 2 : 1) > kMaxCounters) continue;
       order_heads(a, c.ns, c.order);
       const double t = simulate(a, c.ns, c.order, sms, pair);
       if (t < best_t * 0.995) {
@@ -1382,11 +1397,11 @@ extern "C" int df_attn_fwd(const df_attn_args* a, void* stream) {
   }
   if (groups) {
     const int64_t ranks = pair ? 2 : 1;
-    const int64_t cnt_bytes = ((groups * ranks * 4 + 255) / 256) * 256;
     uint8_t* ws = static_cast<uint8_t*>(a->workspace);
-    p.ws_cnt = reinterpret_cast<int32_t*>(ws);
-    p.ws_o = reinterpret_cast<float*>(ws + cnt_bytes);
+    p.ws_o = reinterpret_cast<float*>(ws);
     p.ws_ml = p.ws_o + slots * ranks * 2 * kBM * a->head_dim;
+    // fixed counter region at the end (4-byte aligned; callers pass the same workspace size every launch)
+    p.ws_cnt = reinterpret_cast<int32_t*>(ws + ((a->workspace_bytes - kCntBytes) & ~int64_t(255)));
   }
   int acc = 0;
   for (int r = 0; r < a->num_heads; ++r) {

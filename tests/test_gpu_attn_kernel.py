@@ -129,13 +129,16 @@ def test_hires_c4_full_size_sampled_rows():
     arena.k.normal_()
     arena.v.normal_()
     q = torch.randn(len(ctxs) * hw, width, device=dev).to(torch.bfloat16)
-    out = torch.empty(len(ctxs) * hw, width, device=dev, dtype=torch.bfloat16)
+    out = torch.full((len(ctxs) * hw, width), float("nan"), device=dev, dtype=torch.bfloat16)
     work = [K.HeadWork(arena, arena.allocate(c), c, h, h) for h, c in enumerate(ctxs)]
     scale = 1.0 / math.sqrt(width)
     K.attention(q, out, work, hw, scale)
-    again = torch.empty_like(out)
+    again = torch.full_like(out, float("nan"))
     K.attention(q, again, work, hw, scale)
     torch.cuda.synchronize()
+    for o in (out, again):
+        bad = torch.isnan(o.float()).any(dim=1).nonzero().flatten()
+        assert bad.numel() == 0, (bad.numel(), bad[:8].tolist(), (bad // hw).unique().tolist())
     assert torch.equal(out, again)
     rows = torch.randperm(hw, device=dev)[:256]
     for h, w in enumerate(work):
@@ -144,3 +147,29 @@ def test_hires_c4_full_size_sampled_rows():
         got = out[h * hw:(h + 1) * hw][rows].float()
         err = (got - ref).abs().max().item() / ref.abs().max().item()
         assert err <= 2e-2, (h, err)
+
+
+def test_split_workspace_reuse_across_plans():
+    """Regression: one split workspace serves launches with different split plans.  A launch with few
+    split groups writes partials where a later launch with more groups used to keep its combine
+    counters; with the counters in a fixed region at the end of the workspace every row of the later
+    launch is still combined and written."""
+    from paper_2601_20499_b200 import kernels as K
+
+    torch.manual_seed(3)
+    dev = torch.device("cuda:0")
+
+    def launch(hw, width, ctxs):
+        arena = K.KVArena(sum(K.KVArena.region_rows(c) for c in ctxs), width, dev)
+        arena.k.normal_()
+        arena.v.normal_()
+        q = torch.randn(len(ctxs) * hw, width, device=dev).to(torch.bfloat16)
+        out = torch.full((len(ctxs) * hw, width), float("nan"), device=dev, dtype=torch.bfloat16)
+        work = [K.HeadWork(arena, arena.allocate(c), c, h, h) for h, c in enumerate(ctxs)]
+        K.attention(q, out, work, hw, 1 / math.sqrt(width))
+        torch.cuda.synchronize()
+        return int(torch.isnan(out.float()).any(dim=1).sum().item())
+
+    assert launch(2048, 64, [16 * 2048] * 8) == 0          # 64 split groups, partials right after
+    assert launch(18720, 128, [2 * 18720, 2 * 18720, 6 * 18720]) == 0  # more groups, same workspace
+    assert launch(2048, 64, [16 * 2048] * 8) == 0
