@@ -238,6 +238,7 @@ def attention(
 
 
 _WORKSPACES: dict[tuple[int, int], torch.Tensor] = {}
+_RETIRED_WORKSPACES: list[torch.Tensor] = []
 
 
 def _split_workspace(device: torch.device, stream_handle: int, nbytes: int) -> torch.Tensor:
@@ -249,6 +250,10 @@ def _split_workspace(device: torch.device, stream_handle: int, nbytes: int) -> t
     key = (device.index if device.index is not None else torch.cuda.current_device(), stream_handle or 0)
     ws = _WORKSPACES.get(key)
     if ws is None or ws.numel() < nbytes:
+        if ws is not None:
+            # a captured CUDA graph (StepGraph, Session(graphs=True)) may still launch into the old
+            # buffer: keep it alive instead of returning it to the allocator
+            _RETIRED_WORKSPACES.append(ws)
         ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
         _WORKSPACES[key] = ws
     return ws
