@@ -173,3 +173,47 @@ def test_split_workspace_reuse_across_plans():
     assert launch(2048, 64, [16 * 2048] * 8) == 0          # 64 split groups, partials right after
     assert launch(18720, 128, [2 * 18720, 2 * 18720, 6 * 18720]) == 0  # more groups, same workspace
     assert launch(2048, 64, [16 * 2048] * 8) == 0
+
+
+def test_randomized_ragged_launches_shared_workspace():
+    """30 seeded random launches back to back on one stream (shared split workspace and plan cache):
+    head counts 1-64 over 1-4 arenas, d 64/128, HW 1-5000, ragged contexts from one token to 20 frames,
+    logit scales 0.5-6; every row written, rows sampled against fp32 torch."""
+    import random
+
+    from paper_2601_20499_b200 import kernels as K
+
+    rng = random.Random(11)
+    torch.manual_seed(11)
+    dev = torch.device("cuda:0")
+    for it in range(30):
+        width = rng.choice([64, 128])
+        hw = rng.choice([1, 7, 128, 300, 1000, 2048, 4680, rng.randint(1, 5000)])
+        heads = rng.randint(1, 64 if hw <= 1000 else 12)
+        n_arenas = rng.randint(1, min(4, heads))
+        ctxs = [rng.randint(1, 20) * hw + rng.choice([0, 0, -rng.randint(0, max(0, hw - 1))]) for _ in range(heads)]
+        ctxs = [max(1, c) for c in ctxs]
+        arenas = [K.KVArena(sum(K.KVArena.region_rows(c) for c in ctxs), width, dev) for _ in range(n_arenas)]
+        for a in arenas:
+            a.k.normal_()
+            a.v.normal_()
+        scale_q = rng.choice([0.5, 1.0, 3.0, 6.0])
+        q = (torch.randn(heads * hw, width, device=dev) * scale_q).to(torch.bfloat16)
+        out = torch.full((heads * hw, width), float("nan"), device=dev, dtype=torch.bfloat16)
+        work = []
+        for h, c in enumerate(ctxs):
+            a = arenas[h % n_arenas]
+            work.append(K.HeadWork(a, a.allocate(c), c, h, h))
+        scale = 1.0 / math.sqrt(width)
+        K.attention(q, out, work, hw, scale)
+        torch.cuda.synchronize()
+        assert not torch.isnan(out.float()).any(), (it, width, hw, heads, ctxs[:4])
+        rows = torch.randint(0, hw, (min(hw, 64),), device=dev)
+        for h in rng.sample(range(heads), min(heads, 4)):
+            w = work[h]
+            ref = _ref(q[h * hw:(h + 1) * hw][rows], w.arena.k[w.base_row:w.base_row + w.n_tok],
+                       w.arena.v[w.base_row:w.base_row + w.n_tok], scale)
+            got = out[h * hw:(h + 1) * hw][rows].float()
+            err = (got - ref).abs().max().item() / ref.abs().max().item()
+            assert err <= 2e-2, (it, h, err, width, hw, ctxs[h])
+        del arenas, q, out
