@@ -536,6 +536,63 @@ def reference_arm(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ head-parallel leg (--mode headpar)
+def headpar_arm(args, ws, rank, local):
+    """BASELINE configs[3]: the high-resolution frame (HW 18720, ~720p-class) with its heads sharded over
+    the N GPUs of one box (parallel.HeadParallelSession: H/N heads per rank before classification, LPT
+    rebalance after it, the head-output all-gather fused into the FMHA epilogue over NVLink).  One
+    rollout of --steps AR steps (probe at step 2, 50% dummies) through the fused projections; device
+    time, max over ranks; value = latent frames/s of the one video all ranks produce together."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2601_20499_b200 as df
+    from paper_2601_20499_b200 import _lib
+    from paper_2601_20499_b200.parallel import HeadParallelSession
+
+    dev = torch.device("cuda", local)
+    _lib.require_device(local)
+    hw = 4 * HW
+    ar_steps = max(args.steps, W + 3)
+    Dm = H * D
+    g = torch.Generator(device=dev).manual_seed(21)  # identical weights and frames on every rank
+    weights = [{n: torch.randn(Dm, Dm, device=dev, generator=g) * (0.5 / Dm ** 0.5) for n in ("q", "k", "v", "o")}
+               for _ in range(L)]
+    fg = torch.Generator(device=dev)
+
+    def frames(ar, t):
+        fg.manual_seed(1000 * ar + t)
+        return torch.randn(hw, Dm, device=dev, generator=fg)
+
+    model = df.ProjectedModel(weights, frames, H, D, hw, device=dev)
+    cfg = df.SessionConfig(num_layers=L, num_heads=H, head_dim=D, HW=hw, window_len=W, ar_steps=ar_steps,
+                           denoise_steps=DENOISE, dummy_count=L * H // 2, probe_ar_step=2, subsample_ratio=0.25)
+    if ws == 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    sess = HeadParallelSession(model, cfg, "packed", fused_gather=True, device=dev)
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    sess.run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = barrier_max(e0.elapsed_time(e1), ws)
+    fps = ar_steps * FRAMES_PER_STEP / (ms * 1e-3)
+    line = {"metric": METRIC, "value": fps, "unit": "latent frames/s (one high-resolution video, heads sharded)",
+            "n_gpus": ws, "steps": ar_steps, "warmup": 0, "ms_per_step": ms / ar_steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init Wan attention "
+            "weights, random frames)",
+            "config": {"workload": "configs[3]: Wan-2.1-1.3B attention at HW 18720 (4x tokens/frame), 30 layers x 12 "
+                                   "heads x d128, W 6, 50% dummies via DHP, head-parallel with the fused all-gather",
+                       "HW": hw, "heads_per_rank_before_rebalance": H // ws, "parallelism": f"head-parallel x{ws}"},
+            "rebalance": getattr(sess, "rebalance_stats", None), "gpu_launches": None}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------------ GPU leg
 def gpu_arm(args, ws, rank, local):
     import torch
@@ -700,13 +757,19 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-configs", action="store_true", help="skip the configs[2..3] / SURVEY 8(d) extra timings")
+    ap.add_argument("--mode", default="streams", choices=["streams", "headpar"],
+                    help="streams: independent streams per GPU (default, weak scaling); headpar: configs[3], one "
+                         "high-resolution video with its heads sharded over the GPUs (strong scaling)")
     args = ap.parse_args()
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         reference_arm(args, int(os.environ.get("WORLD_SIZE", "1")), rank)
         return
     ws, rank, local = dist_setup()
-    gpu_arm(args, ws, rank, local)
+    if args.mode == "headpar":
+        headpar_arm(args, ws, rank, local)
+    else:
+        gpu_arm(args, ws, rank, local)
     if ws > 1:
         import torch.distributed as dist
 

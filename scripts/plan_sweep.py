@@ -25,7 +25,8 @@ for name, ctxs in [("6d3s3n", [28080] * 3 + [9360] * 9), ("3d4s5n", [28080] * 5 
     res.append(f"{name} {us:.1f}us {4 * D * HW * sum(ctxs) / us / 1e6:.0f}TF")
 print(" | ".join(res))
 '''
-for piece, split, comb in [(3, 2, 0), (3, 2, 0.75), (3, 2, 1.5), (5, 2, 0.75), (3, 1, 1.0), (2, 1, 1.0)]:
+grid = [(3, 1, 1.0), (2, 1, 1.0), (4, 1, 1.0), (3, 0.5, 1.0), (3, 2, 1.0), (3, 1, 0.5), (3, 1, 1.5), (1, 1, 1.0), (6, 1, 1.0)]
+for piece, split, comb in grid:
     env = dict(os.environ, DF_PLAN_PIECE=str(piece), DF_PLAN_SPLIT=str(split), DF_PLAN_COMBINE=str(comb))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     print(f"piece {piece} split {split} combine {comb}: {r.stdout.strip() or r.stderr[-300:]}", flush=True)
