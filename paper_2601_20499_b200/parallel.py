@@ -303,10 +303,14 @@ class FusedHeadGather:
         for _ in range(2):
             t = symm.empty((rows, width), dtype=torch.bfloat16, device=device)
             h = symm.rendezvous(t, name)
-            peers = [h.get_buffer(r, tuple(t.shape), t.dtype).data_ptr() for r in range(h.world_size) if r != h.rank]
+            # the tensor may sit at an offset inside the symmetric allocation: map the same offset on every rank
+            off = (t.data_ptr() - int(h.buffer_ptrs[h.rank])) // t.element_size()
+            view = lambda r: h.get_buffer(r, tuple(t.shape), t.dtype, off).data_ptr()
+            if view(h.rank) != t.data_ptr():
+                raise ConfigError("symmetric-memory mapping of the gathered output buffer is inconsistent")
             self.bufs.append(t)
             self.handles.append(h)
-            self.peers.append(peers)
+            self.peers.append([view(r) for r in range(h.world_size) if r != h.rank])
 
     def buffer(self, layer: int) -> torch.Tensor:
         return self.bufs[layer % 2]
