@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -107,7 +108,12 @@ struct __align__(64) AttnParams {
 // and the MMA issuer, first kTraceIters kv tiles.  Read with df_trace_fetch.
 constexpr int kTraceIters = 128;
 __device__ unsigned long long g_trace[3][kTraceIters][10];
-__device__ unsigned long long g_cta_time[1024][2];  // clock64 at CTA start / end (per-SM clocks)
+__device__ unsigned long long g_cta_time[1024][4];  // globaltimer ns at CTA start / main-loop end / CTA end, SM id
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #define DF_STAMP(who, it, k)                                                        \
   do {                                                                              \
     if (blockIdx.x == 0 && (it) < kTraceIters) g_trace[who][it][k] = clock64();      \
@@ -203,7 +209,12 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
   }
   if (threadIdx.x == 0) DF_STAMP(2, kTraceIters - 1, 6);
 #ifdef DF_TRACE
-  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_time[blockIdx.x][0] = clock64();
+  if (threadIdx.x == 0 && blockIdx.x < 1024) {
+    g_cta_time[blockIdx.x][0] = gtimer();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_cta_time[blockIdx.x][3] = smid;
+  }
 #endif
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
@@ -479,6 +490,9 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
 
     // ------------------------------------------------------------ epilogue
     if (stamp) DF_STAMP(t, kTraceIters - 1, 6);
+#ifdef DF_TRACE
+    if (threadIdx.x == 128 && blockIdx.x < 1024) g_cta_time[blockIdx.x][1] = gtimer();
+#endif
     mbar_wait(o_full + t, (n_kv - 1) & 1);
     tc_fence_after();
     const int prow = t * kBM + row_local;           // row within the pair
@@ -612,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
   __syncthreads();
   if (threadIdx.x == 0) DF_STAMP(2, kTraceIters - 1, 8);
 #ifdef DF_TRACE
-  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_time[blockIdx.x][1] = clock64();
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_time[blockIdx.x][2] = gtimer();
 #endif
   if (warp == 1) {
     tc_fence_after();
@@ -1151,6 +1165,7 @@ const double kSplitOverhead = env_or("DF_PLAN_SPLIT", 1.0);
 const double kCombinePerPiece = env_or("DF_PLAN_COMBINE", 1.0);
 constexpr double kSingleTileFactor = 0.95;  // last pair with only its first tile valid: no ping-pong, ~as slow as a full pair (clock64 trace)
 constexpr int kMaxSplit = 16;
+const bool kPlanRefine = env_or("DF_PLAN_REFINE", 1.0) != 0.0;  // dev A/B
 
 struct Plan {
   uint8_t ns[DF_MAX_HEADS];
@@ -1252,6 +1267,62 @@ Plan make_plan(const df_attn_args* a, bool allow_split, bool pair) {
         std::memcpy(best.order, c.order, sizeof(c.order));
       }
     }
+  }
+  const double uniform_t = best_t;
+  const Plan uniform = best;
+  if (allow_split && kPlanRefine) {
+    // per-head refinement of the best uniform cap: a few rounds of coordinate descent over each
+    // head's split count (ragged packed layers want e.g. some short heads split to fill the last
+    // wave that the long heads' pieces leave)
+    // Moves: set the split count of the first k heads of a length class (heads with the same
+    // context) to v -- single heads alone rarely help, a packed layer wants e.g. every neighbor
+    // head at 3 pieces AND two of its dummy heads at 3.
+    std::vector<std::vector<int>> classes;
+    for (int h = 0; h < a->num_heads; ++h) {
+      bool placed = false;
+      for (auto& c : classes)
+        if (a->heads[c[0]].n_tok == a->heads[h].n_tok) {
+          c.push_back(h);
+          placed = true;
+          break;
+        }
+      if (!placed) classes.push_back({h});
+    }
+    for (int round = 0; round < 4; ++round) {
+      bool improved = false;
+      for (const auto& cls : classes) {
+        const int tiles = (a->heads[cls[0]].n_tok + 127) / 128;
+        for (int v = 1; v <= std::min(kMaxSplit, tiles); ++v)
+          for (size_t k = 1; k <= cls.size(); ++k) {
+            Plan c = best;
+            bool changed = false;
+            for (size_t i = 0; i < k; ++i) {
+              changed |= c.ns[cls[i]] != v;
+              c.ns[cls[i]] = static_cast<uint8_t>(v);
+            }
+            if (!changed) continue;
+            if (split_groups(a, c.ns, pair, nullptr) * (pair ? 2 : 1) > kMaxCounters) continue;
+            order_heads(a, c.ns, c.order);
+            const double t = simulate(a, c.ns, c.order, sms, pair);
+            if (t < best_t * 0.999) {
+              best_t = t;
+              best = c;
+              improved = true;
+            }
+          }
+      }
+      if (!improved) break;
+    }
+  }
+  if (best_t > uniform_t * 0.98) {  // predicted gains under 2% were not real on the GPU (packed Wan: 193 -> 191)
+    best = uniform;
+    best_t = uniform_t;
+  }
+  if (std::getenv("DF_PLAN_DEBUG")) {
+    std::fprintf(stderr, "plan hw %d heads %d: makespan %.1f (uniform best %.1f) ns:", a->hw, a->num_heads, best_t,
+                 uniform_t);
+    for (int h = 0; h < a->num_heads; ++h) std::fprintf(stderr, " %d/%d", (a->heads[h].n_tok + 127) / 128, best.ns[h]);
+    std::fprintf(stderr, "\n");
   }
   best.ws_bytes = workspace_need(a, best.ns, pair);
   const int nq = (a->hw + item_rows(pair) - 1) / item_rows(pair);
