@@ -152,6 +152,11 @@ DF_API int df_kv_arena_maps(const void* k_base, const void* v_base, int64_t rows
 /* ---- ring manager data movement ---- */
 /* Up to DF_MAX_APPEND_SEGS segments passed by value (one launch). */
 DF_API int df_kv_append(const df_copy_seg* segs, int32_t n_segs, void* stream);
+/* Same copy, launched with programmatic stream serialization: if the kernel
+ * before it on the stream is df_attn_fwd, it may start while that launch's last
+ * wave is still running.  Only for destinations the preceding df_attn_fwd does
+ * not read (e.g. the next layer's ring slots); the Python layer checks this. */
+DF_API int df_kv_append_overlapped(const df_copy_seg* segs, int32_t n_segs, void* stream);
 /* Bulk compaction: segment list already in device memory; chunk_prefix is a
  * device int64 [n_segs+1] exclusive prefix of per-segment 16-byte-chunk
  * counts divided by chunk granularity (see df_kv_pack_plan). */

@@ -130,6 +130,7 @@ _SIGNATURES = {
         [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p],
     ),
     "df_kv_append": (ctypes.c_int, [ctypes.POINTER(CopySeg), ctypes.c_int32, ctypes.c_void_p]),
+    "df_kv_append_overlapped": (ctypes.c_int, [ctypes.POINTER(CopySeg), ctypes.c_int32, ctypes.c_void_p]),
     "df_kv_pack": (
         ctypes.c_int,
         [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p],

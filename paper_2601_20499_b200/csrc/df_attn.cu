@@ -217,6 +217,10 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
   }
 #endif
   if (warp == 1) tmem_alloc(tmem_slot, 512);
+  // Once every CTA of this grid has started, a dependent launched with programmatic
+  // stream serialization (the next layer's df_kv_append, which reads nothing this
+  // kernel writes) may run on the SMs whose CTAs are done: it fills the last wave.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) DF_STAMP(2, kTraceIters - 1, 7);

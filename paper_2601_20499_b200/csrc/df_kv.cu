@@ -156,11 +156,29 @@ static Seg to_seg(const df_copy_seg& s) {
   return d;
 }
 
+bool append_overlap() {  // DF_APPEND_PDL=0 turns the programmatic dependent launch off (dev A/B)
+  static const bool on = [] {
+    const char* env = std::getenv("DF_APPEND_PDL");
+    return !(env && env[0] == '0');
+  }();
+  return on;
+}
+
 }  // namespace dfb
 
 using namespace dfb;
 
+static int kv_append(const df_copy_seg* segs, int32_t n, void* stream, bool overlapped);
+
 extern "C" int df_kv_append(const df_copy_seg* segs, int32_t n, void* stream) {
+  return kv_append(segs, n, stream, false);
+}
+
+extern "C" int df_kv_append_overlapped(const df_copy_seg* segs, int32_t n, void* stream) {
+  return kv_append(segs, n, stream, append_overlap());
+}
+
+static int kv_append(const df_copy_seg* segs, int32_t n, void* stream, bool overlapped) {
   if (n < 0 || n > DF_MAX_APPEND_SEGS || (n > 0 && !segs))
     return set_error(DF_E_ARG, "df_kv_append: n_segs %d outside [0, %d]", n, DF_MAX_APPEND_SEGS);
   if (n == 0) return DF_OK;
@@ -179,8 +197,24 @@ extern "C" int df_kv_append(const df_copy_seg* segs, int32_t n, void* stream) {
   int64_t chunks = (max_vecs + kChunkVecs - 1) / kChunkVecs;
   if (chunks > 65535) chunks = 65535;
   dim3 grid(static_cast<unsigned>(chunks), static_cast<unsigned>(n));
-  df_append_kernel<<<grid, kCopyThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
-  cudaError_t e = cudaGetLastError();
+  // df_kv_append_overlapped: programmatic dependent launch.  When the previous
+  // kernel on the stream is a df_attn_fwd launch (every CTA of which signals
+  // griddepcontrol.launch_dependents as it starts), this copy -- the next layer's
+  // current frame into its ring, which that launch does not read -- runs on the
+  // SMs the FMHA's last wave leaves idle instead of after it drains.  After any
+  // other kernel it starts at that kernel's completion, as a plain launch would.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kCopyThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = overlapped ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, df_append_kernel, p);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("df_append_kernel launch", e);
   return DF_OK;
 }

@@ -138,6 +138,10 @@ def _q_rows(q_heads: torch.Tensor, H: int, hw: int, d: int, width: int, device) 
     return q.reshape(H * hw, width).contiguous()
 
 
+# rings (HeadKVCache ids) read by the last df_attn_fwd launched on each stream
+_LAST_ATTN_RINGS: dict[int, set[int]] = {}
+
+
 @dataclass(frozen=True)
 class OutputTarget:
     """Where a layer's outputs land in a head-parallel session with the fused
@@ -209,9 +213,15 @@ def _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, strea
         pb = K.ProbeBuffers(torch.from_numpy(tab).to(device, non_blocking=False), probe.row_sampled, probe.probe_rows)
     lc = LayerCounters(kernel_calls=calls, key_token_macs=macs, physical_launches=0)
     s = stream if stream is not None else torch.cuda.current_stream(device)
-    # build every launch first so the timed region holds no host work
-    copies = K.prepare_copies([sg[:6] for sg in segs])
+    # build every launch first so the timed region holds no host work.  The staging copy may
+    # overlap the previous FMHA launch on this stream (programmatic dependent launch) unless
+    # that launch read these rings (e.g. the same layer again: its pending slots are rewritten)
+    ring_ids = {id(c) for c in caches}
+    prev = _LAST_ATTN_RINGS.get(s.cuda_stream)
+    overlap = not timed and prev is not None and prev.isdisjoint(ring_ids)
+    copies = K.prepare_copies([sg[:6] for sg in segs], overlapped=overlap)
     attn = K.prepare_attention(q2, out, work, hw, 1.0 / math.sqrt(head_dim), pb, None, s, peers)
+    _LAST_ATTN_RINGS[s.cuda_stream] = ring_ids
     if timed:
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record(s)

@@ -259,15 +259,20 @@ def _split_workspace(device: torch.device, stream_handle: int, nbytes: int) -> t
     return ws
 
 
-def prepare_copies(segs: list[tuple[int, int, int, int, int, int]]) -> list[PreparedLaunch]:
-    """df_kv_append launches (<= DF_MAX_APPEND_SEGS segments each), built ahead of time."""
+def prepare_copies(segs: list[tuple[int, int, int, int, int, int]], overlapped: bool = False) -> list[PreparedLaunch]:
+    """df_kv_append launches (<= DF_MAX_APPEND_SEGS segments each), built ahead of time.
+
+    ``overlapped``: the first launch may start during the previous df_attn_fwd on the stream
+    (df_kv_append_overlapped) -- only when that launch does not read the destinations.
+    """
     out = []
     for i in range(0, len(segs), _lib.DF_MAX_APPEND_SEGS):
         chunk = segs[i : i + _lib.DF_MAX_APPEND_SEGS]
         arr = (_lib.CopySeg * len(chunk))()
         for j, s in enumerate(chunk):
             arr[j].src, arr[j].dst, arr[j].rows, arr[j].src_ld, arr[j].dst_ld, arr[j].row_bytes = s
-        out.append(PreparedLaunch("df_kv_append", (arr, ctypes.c_int32(len(chunk))), (arr,)))
+        fn = "df_kv_append_overlapped" if (overlapped and i == 0) else "df_kv_append"
+        out.append(PreparedLaunch(fn, (arr, ctypes.c_int32(len(chunk))), (arr,)))
     return out
 
 
