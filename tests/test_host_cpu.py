@@ -234,3 +234,28 @@ def test_sweep_cli_config_errors(tmp_path):
     p = tmp_path / "c.json"
     p.write_text(json.dumps({"schema_version": 2, "session": {}}))
     assert S.main(["--config", str(p), "--axis", "context_len", "--out", str(tmp_path / "o.csv")]) == 1
+
+
+def test_batched_step_request_checks_on_host():
+    """batched_step's per-request checks are the single-request step functions' (engine.py:140-195):
+    policy kind for baseline, class count, packing switch, unknown mode -- raised before any launch."""
+    from paper_2601_20499_b200 import engine
+
+    cfg = df.SessionConfig(num_layers=1, num_heads=2, head_dim=64, HW=8, window_len=4, ar_steps=5, dummy_count=1)
+    base = [df.HeadKVCache(df.baseline_policy(cfg)) for _ in range(2)]
+    classes = [df.HeadClass.DUMMY, df.HeadClass.NEIGHBOR]
+    pruned = [df.HeadKVCache(df.derive_policy(c, cfg)) for c in classes]
+    assert engine._request_groups(df.StepRequest("baseline", None, base, []), cfg) == [[0, 1]]
+    assert engine._request_groups(df.StepRequest("packed", None, pruned, [], classes), cfg) == [[0], [1]]
+    assert len(engine._request_groups(df.StepRequest("hma", None, pruned, [], classes), cfg)) == 3
+    with pytest.raises(df.ConfigError):
+        engine._request_groups(df.StepRequest("baseline", None, pruned, []), cfg)
+    with pytest.raises(df.AssignmentError):
+        engine._request_groups(df.StepRequest("packed", None, pruned, [], classes[:1]), cfg)
+    with pytest.raises(df.ConfigError):
+        engine._request_groups(df.StepRequest("bogus", None, pruned, [], classes), cfg)
+    nopack = df.SessionConfig(**{**cfg.__dict__, "packing_enabled": False})
+    with pytest.raises(df.ConfigError):
+        engine._request_groups(df.StepRequest("packed", None, pruned, [], classes), nopack)
+    with pytest.raises(df.ShapeError):
+        df.batched_step([], cfg)
