@@ -1263,6 +1263,12 @@ Plan make_plan(const df_attn_args* a, bool allow_split, bool pair) {
         c.ns[h] = static_cast<uint8_t>(std::min(kMaxSplit, std::max(1, (tiles + cap - 1) / cap)));
       }
       if (split_groups(a, c.ns, pair, nullptr) * (pair ? 2 : 1) > kMaxCounters) continue;
+      {  // more than ~6 pieces per SM: per-piece overheads dominate, not worth simulating
+        const int nq = (a->hw + item_rows(pair) - 1) / item_rows(pair);
+        int64_t items = 0;
+        for (int h = 0; h < a->num_heads; ++h) items += int64_t(nq) * c.ns[h];
+        if (items > 6 * int64_t(sms)) continue;
+      }
       order_heads(a, c.ns, c.order);
       const double t = simulate(a, c.ns, c.order, sms, pair);
       if (t < best_t * 0.995) {
@@ -1274,7 +1280,16 @@ Plan make_plan(const df_attn_args* a, bool allow_split, bool pair) {
   }
   const double uniform_t = best_t;
   const Plan uniform = best;
-  if (allow_split && kPlanRefine) {
+  // Refinement costs up to a few hundred simulations (~10-40 ms of host time per new signature, and a
+  // rollout meets dozens of signatures): skip it when the uniform plan is already within 3% of the
+  // list-scheduling lower bound (all work spread evenly, at one piece per head)
+  double total = 0.0;
+  {
+    const int nq = (a->hw + item_rows(pair) - 1) / item_rows(pair);
+    for (int h = 0; h < a->num_heads; ++h) total += double(nq) * ((a->heads[h].n_tok + 127) / 128 + kPieceOverhead);
+  }
+  const bool near_bound = uniform_t <= 1.03 * total / sms;
+  if (allow_split && kPlanRefine && !near_bound) {
     // per-head refinement of the best uniform cap: a few rounds of coordinate descent over each
     // head's split count (ragged packed layers want e.g. some short heads split to fill the last
     // wave that the long heads' pieces leave)
@@ -1292,11 +1307,12 @@ Plan make_plan(const df_attn_args* a, bool allow_split, bool pair) {
         }
       if (!placed) classes.push_back({h});
     }
-    for (int round = 0; round < 4; ++round) {
+    for (int round = 0; round < 2; ++round) {
       bool improved = false;
       for (const auto& cls : classes) {
         const int tiles = (a->heads[cls[0]].n_tok + 127) / 128;
-        for (int v = 1; v <= std::min(kMaxSplit, tiles); ++v)
+        const int cur = best.ns[cls[0]];
+        for (int v = std::max(1, cur - 2); v <= std::min({kMaxSplit, tiles, 2 * cur + 2}); ++v)
           for (size_t k = 1; k <= cls.size(); ++k) {
             Plan c = best;
             bool changed = false;
@@ -1346,25 +1362,46 @@ PlanCache& plan_cache() {
   return c;
 }
 
+// The cache key is the SORTED context list: a session's layers carry the same multiset of head
+// lengths in different head orders after classification, and a plan depends only on the lengths
+// (the canonical plan's split counts are mapped back through the sort permutation).
 Plan get_plan(const df_attn_args* a, bool allow_split, bool pair) {
+  const int H = a->num_heads;
+  std::vector<int> perm(H);
+  std::iota(perm.begin(), perm.end(), 0);
+  std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return a->heads[x].n_tok > a->heads[y].n_tok; });
   std::vector<int64_t> key;
-  key.reserve(a->num_heads + 5);
+  key.reserve(H + 5);
   key.push_back(a->hw);
   key.push_back(a->head_dim);
   key.push_back(allow_split);
   key.push_back(pair);
   key.push_back(sm_count_cached());
-  for (int i = 0; i < a->num_heads; ++i) key.push_back(a->heads[i].n_tok);
+  for (int i = 0; i < H; ++i) key.push_back(a->heads[perm[i]].n_tok);
+  Plan canon{};
+  bool hit = false;
   PlanCache& pc = plan_cache();
   {
     std::lock_guard<std::mutex> g(pc.mu);
     auto it = pc.map.find(key);
-    if (it != pc.map.end()) return it->second;
+    if (it != pc.map.end()) {
+      canon = it->second;
+      hit = true;
+    }
   }
-  Plan p = make_plan(a, allow_split, pair);
-  std::lock_guard<std::mutex> g(pc.mu);
-  if (pc.map.size() > 4096) pc.map.clear();
-  pc.map.emplace(std::move(key), p);
+  if (!hit) {
+    df_attn_args sorted = *a;
+    std::vector<df_head_desc> heads(H);
+    for (int i = 0; i < H; ++i) heads[i] = a->heads[perm[i]];
+    sorted.heads = heads.data();
+    canon = make_plan(&sorted, allow_split, pair);
+    std::lock_guard<std::mutex> g(pc.mu);
+    if (pc.map.size() > 4096) pc.map.clear();
+    pc.map.emplace(std::move(key), canon);
+  }
+  Plan p = canon;
+  for (int i = 0; i < H; ++i) p.ns[perm[i]] = canon.ns[i];
+  order_heads(a, p.ns, p.order);
   return p;
 }
 
