@@ -30,9 +30,15 @@ def padded_width(head_dim: int) -> int:
     return 64 if head_dim <= 64 else 128
 
 
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream_handle(stream: torch.cuda.Stream | None) -> ctypes.c_void_p:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return ctypes.c_void_p(s.cuda_stream)
+    if stream is not None:
+        return ctypes.c_void_p(stream.cuda_stream)
+    if _RAW_STREAM is not None:  # the current stream's handle without torch.cuda.current_stream()'s Python layers
+        return ctypes.c_void_p(_RAW_STREAM(torch.cuda.current_device()))
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
 class KVArena:

@@ -166,8 +166,21 @@ def _row_bytes(d: int) -> int:
     return ((d + 7) // 8) * 8 * 2
 
 
+def _in_place(block: FrameBlock, st: RingStorage, slot: int) -> bool:
+    """``block`` IS ring slot ``slot`` (df_qkv_project wrote it there): checked on raw pointers, no views."""
+    k, v = block.keys, block.values
+    if not (isinstance(k, torch.Tensor) and isinstance(v, torch.Tensor)) or k.dtype != torch.bfloat16:
+        return False
+    row0 = st.base_row + slot * st.hw
+    step = st.arena.width * 2
+    return (k.data_ptr() == st.arena.k.data_ptr() + row0 * step and v.data_ptr() == st.arena.v.data_ptr() + row0 * step
+            and k.stride(0) == st.arena.width and v.stride(0) == st.arena.width and k.shape[0] == st.hw)
+
+
 def _block_segments(block: FrameBlock, st: RingStorage, slot: int, device) -> list[tuple]:
     """Copy segments (K and V) writing `block` into ring slot `slot`."""
+    if _in_place(block, st, slot):
+        return []  # produced in place: nothing to move
     segs = []
     d = st.head_dim
     width = st.arena.width
@@ -198,6 +211,8 @@ class HeadKVCache:
         self.storage = storage
         self._slot_frame: list[int | None] = [None] * (storage.slots if storage else policy.ring_slots)
         self._staged: tuple | None = None
+        self._views: dict[int, tuple] = {}  # pending-slot views (pending_view), per storage
+        self._views_of: RingStorage | None = None
         for b in blocks or []:
             self.append_and_evict(b)
 
@@ -251,8 +266,14 @@ class HeadKVCache:
         copy at all.
         """
         st = self.ensure_storage(hw, head_dim, device)
-        r = st.rows(self.pending_slot)
-        return st.arena.k[r, :head_dim], st.arena.v[r, :head_dim]
+        slot = self.pending_slot
+        views = self._views.get(slot) if self._views_of is st else None
+        if views is None:  # views of a slot are reused across layers' denoise iterations
+            if self._views_of is not st:
+                self._views, self._views_of = {}, st
+            r = st.rows(slot)
+            views = self._views[slot] = (st.arena.k[r, :head_dim], st.arena.v[r, :head_dim])
+        return views
 
     def past_tokens(self) -> int:
         return len(self) * (self.storage.hw if self.storage else 0)
@@ -274,9 +295,12 @@ class HeadKVCache:
         return codes
 
     # ------------------------------------------------------------ updates
+    def _newest(self) -> int | None:
+        return max((f for f in self._slot_frame if f is not None), default=None)
+
     def check_current(self, frame_id: int) -> None:
-        ids = self.frame_ids
-        if ids and frame_id <= ids[-1]:
+        newest = self._newest()
+        if newest is not None and frame_id <= newest:
             raise OrderingError(f"current frame {frame_id} not newer than cache")
 
     def stage_segments(self, block: FrameBlock, device=None) -> list[tuple]:
