@@ -210,7 +210,10 @@ def _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, strea
         tab = np.ones((H, max_slots), dtype=np.uint8)
         for h, c in enumerate(caches):
             tab[h, : c.storage.slots] = c.region_codes()
-        pb = K.ProbeBuffers(torch.from_numpy(tab).to(device, non_blocking=False), probe.row_sampled, probe.probe_rows)
+        # pinned + non_blocking: a pageable upload would wait for every queued launch (one host/device
+        # serialisation per probe layer)
+        pb = K.ProbeBuffers(torch.from_numpy(tab).pin_memory().to(device, non_blocking=True), probe.row_sampled,
+                            probe.probe_rows)
     lc = LayerCounters(kernel_calls=calls, key_token_macs=macs, physical_launches=0)
     s = stream if stream is not None else torch.cuda.current_stream(device)
     # build every launch first so the timed region holds no host work.  The staging copy may
@@ -509,6 +512,7 @@ class Session:
         self._phys_last: list[int] = []
         self._probe_requests: dict[tuple[int, int], set[float]] = {}
         self._probe_tables: dict[tuple[int, int, float], np.ndarray] = {}
+        self._row_flags: dict[float, torch.Tensor] = {}
         self._classify_at: tuple[int, int] | None = None
         if mode != "baseline" and config.dummy_count > 0 and config.probe_ar_step < config.ar_steps:
             self._classify_at = self._probe_key(None)
@@ -678,11 +682,13 @@ class Session:
 
     def _probe_buffers(self, ratio: float) -> ProbeRequest:
         cfg = self.config
-        rows = subsample_rows(cfg.HW, ratio)
-        flags = torch.zeros(cfg.HW, dtype=torch.uint8)
-        flags[torch.from_numpy(rows)] = 1
-        return ProbeRequest(flags.to(self.device), torch.zeros(len(self.head_range), cfg.HW, 3, dtype=torch.float32,
-                                                                device=self.device))
+        flags = self._row_flags.get(ratio)
+        if flags is None:  # once per ratio (a pageable upload per layer would serialise host and device)
+            rows = subsample_rows(cfg.HW, ratio)
+            host = torch.zeros(cfg.HW, dtype=torch.uint8)
+            host[torch.from_numpy(rows)] = 1
+            flags = self._row_flags[ratio] = host.to(self.device)
+        return ProbeRequest(flags, torch.zeros(len(self.head_range), cfg.HW, 3, dtype=torch.float32, device=self.device))
 
     def _finalize_probe(self, key, ratio, per_layer: list[ProbeRequest]) -> None:
         tables = []
