@@ -482,6 +482,45 @@ def kernel_configs(df, dev, bf16_peak):
     return res
 
 
+def batched_streams(df, cfg, dev, gen, packed, inputs, classes, args, B=4):
+    """BASELINE configs[4] at the step level: B independent streams per GPU, each with its own warm packed
+    rings and inputs, every layer's B requests in ONE FMHA launch through the public batched_step."""
+    import torch
+
+    caches_b, inputs_b = [packed], [inputs]
+    pols = [df.derive_policy(df.HeadClass(ASSIGN[i % H]), cfg) for i in range(L * H)]
+    for b in range(1, B):
+        base, _ = build_caches(df, cfg, dev, gen)
+        new = df.rebuild_caches([c for layer in base for c in layer], pols)
+        caches_b.append([new[l * H:(l + 1) * H] for l in range(L)])
+        inputs_b.append([tuple(torch.randn(H, HW, D, device=dev, generator=gen).to(torch.bfloat16) for _ in range(3))
+                         for _ in range(L)])
+        del base
+        torch.cuda.empty_cache()
+    # the streams' Q of a layer back to back in one allocation (as a batched projection would write it):
+    # batched_step then launches on it without a gather copy
+    q_all = [torch.stack([inputs_b[b][layer][0] for b in range(B)]) for layer in range(L)]
+
+    def step():
+        for layer in range(L):
+            reqs = []
+            for b in range(B):
+                _, k, v = inputs_b[b][layer]
+                q = q_all[layer][b]
+                reqs.append(df.StepRequest("packed", q, caches_b[b][layer],
+                                           [df.FrameBlock(W, k[h], v[h]) for h in range(H)], classes))
+            df.batched_step(reqs, cfg, timed=False)
+        return []
+
+    t, _ = time_steps(step, max(3, args.steps // 2), args.warmup)
+    res = {"streams": B, "ms_per_step": t, "fps_all_streams": B * FRAMES_PER_STEP / (DENOISE * t * 1e-3),
+           "us_per_layer_per_stream": t * 1e3 / L / B,
+           "path": "per layer ONE batched_step over the B streams' requests (4 arenas, 48 heads per FMHA launch)"}
+    del caches_b, inputs_b, q_all
+    torch.cuda.empty_cache()
+    return res
+
+
 def rollout_c3(df, dev, ar_steps=40):
     """BASELINE configs[2]: a whole Wan-shape rollout through the public Session -- fused QKV projection ->
     FMHA -> out-projection per layer, probe with the DHP epilogue at AR step 2 (ratio 0.25), greedy
@@ -698,6 +737,7 @@ def gpu_arm(args, ws, rank, local):
     if not args.no_configs:
         extra = kernel_configs(df, dev, bf16_peak)
         extra["rollout_c3"] = rollout_c3(df, dev)
+        extra["streams4_batched_step_c5"] = batched_streams(df, cfg, dev, gen, packed, inputs, classes, args)
 
     # e2e through the public API with host buffers
     pinned = [tuple(x.cpu().pin_memory() for x in layer) for layer in inputs]

@@ -312,6 +312,22 @@ def _request_groups(r: StepRequest, config: SessionConfig) -> list[list[int]]:
             [h for h, c in enumerate(classes) if c is HeadClass.NEIGHBOR]]
 
 
+def _adjacent_rows(qs: list[torch.Tensor]) -> torch.Tensor | None:
+    """One [sum rows, width] view over row blocks that sit back to back in memory (e.g. the streams'
+    Q as slices of one batched tensor), else None."""
+    q0 = qs[0]
+    nxt = q0.data_ptr()
+    for q in qs:
+        if not q.is_contiguous() or q.data_ptr() != nxt or q.dtype != q0.dtype or q.shape[1] != q0.shape[1]:
+            return None
+        nxt += q.numel() * q.element_size()
+    rows = sum(q.shape[0] for q in qs)
+    end = q0.storage_offset() + rows * q0.shape[1]
+    if end > q0.untyped_storage().nbytes() // q0.element_size():
+        return None
+    return q0.as_strided((rows, q0.shape[1]), (q0.shape[1], 1))
+
+
 def batched_step(requests: Sequence[StepRequest], config: SessionConfig, *, stream=None, timed: bool = True):
     """Several independent sessions' layers (SURVEY 8(e) / BASELINE configs[4]: a batch of video streams
     on one GPU) in ONE ragged FMHA launch (more launches only past DF_MAX_HEADS heads or DF_MAX_ARENAS
@@ -363,10 +379,16 @@ def batched_step(requests: Sequence[StepRequest], config: SessionConfig, *, stre
             work += [K.HeadWork(c.storage.arena, c.storage.base_row, n_tok[h], base + h, base + h)
                      for h, c in enumerate(r.caches)]
             base += len(r.caches)
-        q2 = qs[0] if len(qs) == 1 else torch.cat(qs, 0)
+        q2 = _adjacent_rows(qs) if len(qs) > 1 else qs[0]
+        if q2 is None:  # requests' Q not laid out back to back in one allocation: gather them
+            q2 = torch.cat(qs, 0)
         out = torch.empty(base * hw, d8, dtype=torch.bfloat16, device=device)
-        copies = K.prepare_copies([sg[:6] for sg in segs])
+        ring_ids = {id(c) for r in requests for c in r.caches}
+        prev = _LAST_ATTN_RINGS.get(s.cuda_stream)
+        overlap = not timed and prev is not None and prev.isdisjoint(ring_ids)
+        copies = K.prepare_copies([sg[:6] for sg in segs], overlapped=overlap)
         attn = K.prepare_attention(q2, out, work, hw, 1.0 / math.sqrt(d), None, None, s)
+        _LAST_ATTN_RINGS[s.cuda_stream] = ring_ids
         if timed:
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
             ev[0].record(s)
