@@ -138,10 +138,6 @@ def _q_rows(q_heads: torch.Tensor, H: int, hw: int, d: int, width: int, device) 
     return q.reshape(H * hw, width).contiguous()
 
 
-# rings (HeadKVCache ids) read by the last df_attn_fwd launched on each stream
-_LAST_ATTN_RINGS: dict[int, set[int]] = {}
-
-
 @dataclass(frozen=True)
 class OutputTarget:
     """Where a layer's outputs land in a head-parallel session with the fused
@@ -217,14 +213,10 @@ def _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, strea
     lc = LayerCounters(kernel_calls=calls, key_token_macs=macs, physical_launches=0)
     s = stream if stream is not None else torch.cuda.current_stream(device)
     # build every launch first so the timed region holds no host work.  The staging copy may
-    # overlap the previous FMHA launch on this stream (programmatic dependent launch) unless
-    # that launch read these rings (e.g. the same layer again: its pending slots are rewritten)
-    ring_ids = {id(c) for c in caches}
-    prev = _LAST_ATTN_RINGS.get(s.cuda_stream)
-    overlap = not timed and prev is not None and prev.isdisjoint(ring_ids)
-    copies = K.prepare_copies([sg[:6] for sg in segs], overlapped=overlap)
+    # overlap the previous FMHA launch on this stream (programmatic dependent launch) when the
+    # two touch disjoint bytes -- checked when the copy launches (kernels.PreparedLaunch)
+    copies = K.prepare_copies([sg[:6] for sg in segs], overlapped=not timed)
     attn = K.prepare_attention(q2, out, work, hw, 1.0 / math.sqrt(head_dim), pb, None, s, peers)
-    _LAST_ATTN_RINGS[s.cuda_stream] = ring_ids
     if timed:
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record(s)
@@ -383,12 +375,8 @@ def batched_step(requests: Sequence[StepRequest], config: SessionConfig, *, stre
         if q2 is None:  # requests' Q not laid out back to back in one allocation: gather them
             q2 = torch.cat(qs, 0)
         out = torch.empty(base * hw, d8, dtype=torch.bfloat16, device=device)
-        ring_ids = {id(c) for r in requests for c in r.caches}
-        prev = _LAST_ATTN_RINGS.get(s.cuda_stream)
-        overlap = not timed and prev is not None and prev.isdisjoint(ring_ids)
-        copies = K.prepare_copies([sg[:6] for sg in segs], overlapped=overlap)
+        copies = K.prepare_copies([sg[:6] for sg in segs], overlapped=not timed)
         attn = K.prepare_attention(q2, out, work, hw, 1.0 / math.sqrt(d), None, None, s)
-        _LAST_ATTN_RINGS[s.cuda_stream] = ring_ids
         if timed:
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
             ev[0].record(s)

@@ -6,6 +6,7 @@ computes on the CPU: a missing extension or device raises.
 
 from __future__ import annotations
 
+import bisect
 import ctypes
 import math
 import os
@@ -113,14 +114,59 @@ class ProbeBuffers:
     probe_rows: torch.Tensor  # float32 [heads, hw, 3]
 
 
-class PreparedLaunch:
-    """A fully built df_attn_fwd / df_kv_append call: launching is one C call."""
+def _merge(ranges: list[tuple[int, int]]) -> tuple[list[int], list[int]]:
+    """Sorted, merged [lo, hi) byte ranges as two parallel lists."""
+    los: list[int] = []
+    his: list[int] = []
+    for lo, hi in sorted(r for r in ranges if r[1] > r[0]):
+        if his and lo <= his[-1]:
+            his[-1] = max(his[-1], hi)
+        else:
+            los.append(lo)
+            his.append(hi)
+    return los, his
 
-    def __init__(self, fn: str, args: tuple, keep: tuple):
+
+def _hits(merged: tuple[list[int], list[int]], ranges: list[tuple[int, int]]) -> bool:
+    los, his = merged
+    for lo, hi in ranges:
+        i = bisect.bisect_right(los, lo) - 1
+        if (i >= 0 and his[i] > lo) or (i + 1 < len(los) and los[i + 1] < hi):
+            return True
+    return False
+
+
+# byte footprint of the last df_attn_fwd launched on each stream: (touched, written), merged
+_LAST_FMHA: dict[int, tuple[tuple[list[int], list[int]], tuple[list[int], list[int]]]] = {}
+
+
+class PreparedLaunch:
+    """A fully built df_attn_fwd / df_kv_append call: launching is one C call.
+
+    ``touched`` / ``written`` (df_attn_fwd): the byte ranges the launch reads or writes / writes.
+    ``reads`` / ``writes`` (a df_kv_append_overlapped candidate): the copy's source and
+    destination ranges.  The overlapped variant may start while the previous df_attn_fwd on the
+    stream still runs, so it is used only when, at launch time, that FMHA's footprint is
+    disjoint from what the copy writes and its writes are disjoint from what the copy reads;
+    otherwise the plain, fully serialised df_kv_append runs.
+    """
+
+    def __init__(self, fn: str, args: tuple, keep: tuple, touched=None, written=None, reads=None, writes=None):
         self.fn, self.args, self.keep = fn, args, keep
+        self.touched = _merge(touched) if touched is not None else None
+        self.written = _merge(written) if written is not None else None
+        self.reads, self.writes = reads, writes
 
     def launch(self, stream: torch.cuda.Stream | None = None) -> None:
-        _lib.call(self.fn, *self.args, _stream_handle(stream))
+        h = _stream_handle(stream)
+        fn = self.fn
+        if self.writes is not None:
+            last = _LAST_FMHA.get(h.value or 0)
+            if last is None or _hits(last[0], self.writes) or _hits(last[1], self.reads):
+                fn = "df_kv_append"
+        elif self.touched is not None:
+            _LAST_FMHA[h.value or 0] = (self.touched, self.written)
+        _lib.call(fn, *self.args, h)
 
 
 def prepare_attention(
@@ -225,7 +271,29 @@ def prepare_attention(
         ws = _split_workspace(q.device, _stream_handle(stream).value, need.value)
         args.workspace = ws.data_ptr()
         args.workspace_bytes = ws.numel()
-    return [PreparedLaunch("df_attn_fwd", (ctypes.byref(args),), (args, descs, maps_buf, ws, q, out, probe, peers))]
+    written = [_span(out)]
+    touched = [_span(q)]
+    for w in work:
+        # the last kv tile of a head is read whole (TMA box of 128 rows), masked in-kernel
+        rows = min(-(-max(w.n_tok, 1) // 128) * 128, w.arena.rows - w.base_row)
+        lo = w.base_row * w.arena.width * 2
+        for plane in (w.arena.k, w.arena.v):
+            touched.append((plane.data_ptr() + lo, plane.data_ptr() + lo + rows * w.arena.width * 2))
+    if probe is not None:
+        touched += [_span(probe.region_of_slot), _span(probe.row_sampled)]
+        written.append(_span(probe.probe_rows))
+    if ws is not None:
+        written.append(_span(ws))
+    return [PreparedLaunch("df_attn_fwd", (ctypes.byref(args),), (args, descs, maps_buf, ws, q, out, probe, peers),
+                           touched=touched + written, written=written)]
+
+
+def _span(t: torch.Tensor) -> tuple[int, int]:
+    """[lo, hi) bytes a strided tensor view can touch."""
+    if t.numel() == 0:
+        return (t.data_ptr(), t.data_ptr())
+    last = sum((n - 1) * st for n, st in zip(t.shape, t.stride()))
+    return (t.data_ptr(), t.data_ptr() + (last + 1) * t.element_size())
 
 
 def attention(
@@ -269,7 +337,8 @@ def prepare_copies(segs: list[tuple[int, int, int, int, int, int]], overlapped: 
     """df_kv_append launches (<= DF_MAX_APPEND_SEGS segments each), built ahead of time.
 
     ``overlapped``: the first launch may start during the previous df_attn_fwd on the stream
-    (df_kv_append_overlapped) -- only when that launch does not read the destinations.
+    (df_kv_append_overlapped); PreparedLaunch.launch checks, at launch time, that the two do not
+    touch the same bytes and falls back to the serialised df_kv_append when they might.
     """
     out = []
     for i in range(0, len(segs), _lib.DF_MAX_APPEND_SEGS):
@@ -277,8 +346,13 @@ def prepare_copies(segs: list[tuple[int, int, int, int, int, int]], overlapped: 
         arr = (_lib.CopySeg * len(chunk))()
         for j, s in enumerate(chunk):
             arr[j].src, arr[j].dst, arr[j].rows, arr[j].src_ld, arr[j].dst_ld, arr[j].row_bytes = s
-        fn = "df_kv_append_overlapped" if (overlapped and i == 0) else "df_kv_append"
-        out.append(PreparedLaunch(fn, (arr, ctypes.c_int32(len(chunk))), (arr,)))
+        if overlapped and i == 0:
+            reads = [(s[0], s[0] + (s[2] - 1) * s[3] + s[5]) for s in chunk if s[2] > 0]
+            writes = [(s[1], s[1] + (s[2] - 1) * s[4] + s[5]) for s in chunk if s[2] > 0]
+            out.append(PreparedLaunch("df_kv_append_overlapped", (arr, ctypes.c_int32(len(chunk))), (arr,),
+                                      reads=reads, writes=writes))
+        else:
+            out.append(PreparedLaunch("df_kv_append", (arr, ctypes.c_int32(len(chunk))), (arr,)))
     return out
 
 

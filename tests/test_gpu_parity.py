@@ -408,6 +408,9 @@ _PDL_SCRIPT = r"""
 import math, os, sys, torch
 sys.path.insert(0, sys.argv[1])
 import paper_2601_20499_b200 as df
+from paper_2601_20499_b200 import _lib, kernels as K
+names, _call = [], _lib.call
+_lib.call = lambda fn, *a: (names.append(fn), _call(fn, *a))[1]
 dev = torch.device("cuda:0")
 L, H, HW, d, W = 12, 6, 2048, 128, 6
 cfg = df.SessionConfig(num_layers=L, num_heads=H, head_dim=d, HW=HW, window_len=W, ar_steps=W + 2, dummy_count=2 * L)
@@ -425,6 +428,7 @@ for layer in range(L):
         caches.append(c)
     caches = df.rebuild_caches(caches, [df.derive_policy(c, cfg) for c in classes])
     layers.append((caches, rnd(H, HW, d), [df.FrameBlock(W, rnd(HW, d), rnd(HW, d)) for _ in range(H)]))
+names.clear()  # the cache set-up above stages frames with plain copies
 outs = []
 for rep in range(3):  # several passes: layer 0 of a pass follows layer L-1 (disjoint rings, overlapped copy)
     for caches, q, blocks in layers:
@@ -433,9 +437,21 @@ for rep in range(3):  # several passes: layer 0 of a pass follows layer L-1 (dis
     # the same layer twice in a row: its pending slots are rewritten, so this copy must not overlap
     o, _ = df.packed_step(layers[0][1], layers[0][0], layers[0][2], classes, cfg, timed=False)
     outs.append(o)
+# an FMHA launched straight through kernels.attention over layer 1's rings, then layer 1's step:
+# its staging copy rewrites rows that FMHA reads, so it must not overlap it
+caches1, q1, blocks1 = layers[1]
+junk = torch.empty(H * HW, d, dtype=torch.bfloat16, device=dev)
+K.attention(q1.reshape(H * HW, d).contiguous(), junk,
+            [K.HeadWork(c.storage.arena, c.storage.base_row, c.storage.slots * HW, h, h) for h, c in enumerate(caches1)],
+            HW, 1.0 / math.sqrt(d))
+o, _ = df.packed_step(q1, caches1, blocks1, classes, cfg, timed=False)
+outs.append(o)
 torch.cuda.synchronize()
-torch.save([o.cpu() for o in outs], sys.argv[2])
+torch.save(([o.cpu() for o in outs], [n for n in names if n.startswith("df_kv_append")]), sys.argv[2])
 """
+
+
+L_PDL = 12
 
 
 def test_overlapped_staging_copy_matches_serialized(tmp_path):
@@ -454,6 +470,11 @@ def test_overlapped_staging_copy_matches_serialized(tmp_path):
         subprocess.run([_sys.executable, str(script), root, str(tmp_path / f"o{v}.pt")], check=True,
                        env=dict(os.environ, DF_APPEND_PDL=v))
         res[v] = torch.load(tmp_path / f"o{v}.pt")
-    assert len(res["1"]) == len(res["0"]) == 39
-    for a, b in zip(res["1"], res["0"]):
+    (o1, copies), (o0, _) = res["1"], res["0"]
+    assert len(o1) == len(o0) == 40
+    for a, b in zip(o1, o0):
         assert torch.equal(a, b)
+    # per pass: layer 0 follows no FMHA or the repeat of layer 0 (plain), layers 1..11 and the repeat
+    # (after layer 11) overlap; the step after the direct FMHA over its own rings is plain
+    plain, over = "df_kv_append", "df_kv_append_overlapped"
+    assert copies == ([plain] + [over] * L_PDL) * 3 + [plain]
