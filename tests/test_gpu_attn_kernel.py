@@ -217,3 +217,49 @@ def test_randomized_ragged_launches_shared_workspace():
             err = (got - ref).abs().max().item() / ref.abs().max().item()
             assert err <= 2e-2, (it, h, err, width, hw, ctxs[h])
         del arenas, q, out
+
+
+@pytest.mark.parametrize("pair", [False, True])
+def test_attention_writes_only_its_rows(pair):
+    """Bounds check of df_attn_fwd (compute-sanitizer is not available on the GPU pool): the
+    output is a strided view with guard rows around it and gaps between the heads it names (o_head
+    permuted, every other slot skipped); Q and both K/V planes must come back bit-identical, every
+    guard byte untouched, the split-KV combine counters back at zero, and the written rows right."""
+    from paper_2601_20499_b200 import kernels as K
+
+    torch.manual_seed(5)
+    dev = torch.device("cuda:0")
+    width, hw, G = 128, 700, 37
+    ctxs = [60000, 130, 4000, 1, 9360]  # long head: split-KV partials + in-kernel combine
+    H = len(ctxs)
+    arena = K.KVArena(sum(K.KVArena.region_rows(c) for c in ctxs) + 256, width, dev)
+    arena.k.normal_()
+    arena.v.normal_()
+    q = (torch.randn(H * hw, width, device=dev) * 2).to(torch.bfloat16)
+    o_heads = [8, 0, 4, 2, 6]  # out has 2H-1 head slots; odd slots are gaps
+    q_heads = [3, 1, 4, 0, 2]
+    big = torch.full((G + (2 * H - 1) * hw + G, width + 40), 7.0, device=dev, dtype=torch.bfloat16)
+    out = big[G:G + (2 * H - 1) * hw, :width]
+    work = [K.HeadWork(arena, arena.allocate(c), c, q_heads[h], o_heads[h]) for h, c in enumerate(ctxs)]
+    k0, v0, q0 = arena.k.clone(), arena.v.clone(), q.clone()
+    stream = torch.cuda.current_stream()
+    launches = K.prepare_attention(q, out, work, hw, 1 / math.sqrt(width), pair=pair, stream=stream)
+    for launch in launches:
+        launch.launch(stream)
+    torch.cuda.synchronize()
+    assert torch.equal(arena.k, k0) and torch.equal(arena.v, v0) and torch.equal(q, q0)
+    written = torch.zeros(big.shape[0], dtype=torch.bool, device=dev)
+    for o in o_heads:
+        written[G + o * hw:G + (o + 1) * hw] = True
+    assert bool((big[~written] == 7.0).all())
+    assert bool((big[:, width:] == 7.0).all())
+    ws = launches[0].keep[3]
+    if ws is not None:  # the combine returns its counters to zero for the next launch
+        cnt = (ws.numel() - 64 * 1024) & ~255
+        assert int(ws[cnt:cnt + 64 * 1024].count_nonzero()) == 0
+    rows = torch.randint(0, hw, (48,), device=dev)
+    for h, w in enumerate(work):
+        ref = _ref(q[w.q_head * hw:(w.q_head + 1) * hw][rows], arena.k[w.base_row:w.base_row + w.n_tok],
+                   arena.v[w.base_row:w.base_row + w.n_tok], 1 / math.sqrt(width))
+        got = out[w.o_head * hw:(w.o_head + 1) * hw][rows].float()
+        assert float((got - ref).abs().max() / ref.abs().max()) <= 2e-2, h
