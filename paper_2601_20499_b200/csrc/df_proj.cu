@@ -90,9 +90,22 @@ struct ProjParams {
 
 // One 32-column chunk (accumulator registers r, thread = row `lane` of the
 // warp's 32 rows starting at tile row `row0`).
+// The residual rows of one out-projection chunk (x[row0 .. row0+31][n0 .. n0+31], fp32), four rows
+// x 128 B per warp instruction.  Issued one chunk ahead of its use -- the first chunk of a tile
+// before the accumulator is ready -- so the epilogue does not stall on HBM latency per chunk.
+__device__ __forceinline__ void load_residual(const ProjParams& p, int lane, int row0, int n0, float4 (&xv)[8]) {
+  if (n0 >= p.n) return;
+  const int piece = lane & 7;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int row = row0 + 4 * k + (lane >> 3);
+    if (row < p.m) xv[k] = *reinterpret_cast<const float4*>(p.x + static_cast<int64_t>(row) * p.out_ld + n0 + 4 * piece);
+  }
+}
+
 template <int kEpi>
 __device__ __forceinline__ void epilogue_chunk(const ProjParams& p, uint8_t* stg, int lane, int row0, int n0,
-                                               const uint32_t (&r)[32]) {
+                                               const uint32_t (&r)[32], const float4 (&xv)[8]) {
   constexpr int kRow = StageRow<kEpi>::kBytes;
   if constexpr (kEpi == kEpiQKV) {
     uint4* srow = reinterpret_cast<uint4*>(stg + lane * kRow);
@@ -140,12 +153,6 @@ __device__ __forceinline__ void epilogue_chunk(const ProjParams& p, uint8_t* stg
     __syncwarp();
     if (n0 < p.n) {
       const int piece = lane & 7;
-      float4 xv[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int row = row0 + 4 * k + (lane >> 3);
-        if (row < p.m) xv[k] = *reinterpret_cast<const float4*>(p.x + static_cast<int64_t>(row) * p.out_ld + n0 + 4 * piece);
-      }
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int rl = 4 * k + (lane >> 3);
@@ -169,6 +176,25 @@ __device__ __forceinline__ void epilogue_chunk(const ProjParams& p, uint8_t* stg
       }
     }
     __syncwarp();
+  }
+}
+
+// Drain one accumulator tile (this warp's kPer 32-column chunks of its 32 rows).  xv[c] holds the
+// residual of chunk c on entry; as each chunk is consumed, its slot is refilled with chunk c of the
+// next tile (next_row0 / next_n0, when has_next), which then has a whole mainloop to arrive.
+template <int BN, int kEpi>
+__device__ __forceinline__ void drain_tile(const ProjParams& p, uint8_t* stg, int lane, uint32_t taddr, int row0,
+                                           int n0, float4 (&xv)[BN / 64][8], bool has_next, int next_row0,
+                                           int next_n0) {
+  constexpr int kPer = BN / 64;
+#pragma unroll
+  for (int c = 0; c < kPer; ++c) {
+    uint32_t r[32];
+    tmem_ld32(taddr + c * 32, r);
+    tmem_wait_ld();
+    epilogue_chunk<kEpi>(p, stg, lane, row0, n0 + c * 32, r, xv[c]);
+    if constexpr (kEpi == kEpiOut)
+      if (has_next) load_residual(p, lane, next_row0, next_n0 + c * 32, xv[c]);
   }
 }
 
@@ -272,24 +298,20 @@ __global__ void __launch_bounds__(kPThreads, 1) df_proj_kernel(const __grid_cons
     uint8_t* stg = smem + C::kStgOff + (warp - 2) * C::kStgWarp;
     int acc = 0;
     uint32_t acc_phase = 0;
+    float4 xv[kPer][8];
+    auto tile_row0 = [&](int t) { return (t % p.m_tiles) * kPBM + quad * 32; };
+    auto tile_n0 = [&](int t) { return (t / p.m_tiles) * BN + c0 * 32; };
+    if constexpr (kEpi == kEpiOut)
+      if (static_cast<int>(blockIdx.x) < p.tiles)
+#pragma unroll
+        for (int c = 0; c < kPer; ++c) load_residual(p, lane, tile_row0(blockIdx.x), tile_n0(blockIdx.x) + c * 32, xv[c]);
     for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
-      const int mb = tile % p.m_tiles;
-      const int nb = tile / p.m_tiles;
+      const int next = tile + static_cast<int>(gridDim.x);
       mbar_wait(acc_full + acc, acc_phase);
       tc_fence_after();
-      const int row0 = mb * kPBM + quad * 32;
-      const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(quad * 32) << 16);
-#pragma unroll 1
-      for (int c = 0; c < kPer; ++c) {
-        uint32_t r[32];
-        tmem_ld32(taddr + (c0 + c) * 32, r);
-        tmem_wait_ld();
-#ifndef DF_PROJ_DIAG
-        epilogue_chunk<kEpi>(p, stg, lane, row0, nb * BN + (c0 + c) * 32, r);
-#else
-        if (row0 < 0) epilogue_chunk<kEpi>(p, stg, lane, row0, nb * BN + (c0 + c) * 32, r);
-#endif
-      }
+      const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(quad * 32) << 16) + c0 * 32;
+      drain_tile<BN, kEpi>(p, stg, lane, taddr, tile_row0(tile), tile_n0(tile), xv, next < p.tiles, tile_row0(next),
+                           tile_n0(next));
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(acc_empty + acc);
@@ -439,20 +461,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPThreads, 1)
     const uint32_t leader_acc_empty = mapa_shared(smem_u32(acc_empty), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
+    float4 xv[kPer][8];
+    auto tile_row0 = [&](int t) { return (t % p.m_tiles) * 2 * kPBM + static_cast<int>(crank) * kPBM + quad * 32; };
+    auto tile_n0 = [&](int t) { return (t / p.m_tiles) * BN + c0 * 32; };
+    if constexpr (kEpi == kEpiOut)
+      if (cid < p.tiles)
+#pragma unroll
+        for (int c = 0; c < kPer; ++c) load_residual(p, lane, tile_row0(cid), tile_n0(cid) + c * 32, xv[c]);
     for (int tile = cid; tile < p.tiles; tile += nclusters) {
-      const int mb = tile % p.m_tiles;
-      const int nb = tile / p.m_tiles;
+      const int next = tile + nclusters;
       mbar_wait_cluster(acc_full + acc, acc_phase);
       tc_fence_after();
-      const int row0 = mb * 2 * kPBM + static_cast<int>(crank) * kPBM + quad * 32;
-      const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(quad * 32) << 16);
-#pragma unroll 1
-      for (int c = 0; c < kPer; ++c) {
-        uint32_t r[32];
-        tmem_ld32(taddr + (c0 + c) * 32, r);
-        tmem_wait_ld();
-        epilogue_chunk<kEpi>(p, stg, lane, row0, nb * BN + (c0 + c) * 32, r);
-      }
+      const uint32_t taddr = tmem + acc * BN + (static_cast<uint32_t>(quad * 32) << 16) + c0 * 32;
+      drain_tile<BN, kEpi>(p, stg, lane, taddr, tile_row0(tile), tile_n0(tile), xv, next < p.tiles, tile_row0(next),
+                           tile_n0(next));
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_acc_empty + acc * 8);
