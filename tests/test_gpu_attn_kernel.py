@@ -263,3 +263,48 @@ def test_attention_writes_only_its_rows(pair):
                    arena.v[w.base_row:w.base_row + w.n_tok], 1 / math.sqrt(width))
         got = out[w.o_head * hw:(w.o_head + 1) * hw][rows].float()
         assert float((got - ref).abs().max() / ref.abs().max()) <= 2e-2, h
+
+
+def test_attention_over_launch_limits_splits_and_c_abi_rejects():
+    """More heads than DF_MAX_HEADS and more arenas than DF_MAX_ARENAS: prepare_attention splits the
+    list into contiguous launches (results as one launch); the C ABI itself rejects an over-long
+    descriptor table with DF_E_SHAPE instead of reading past its arrays."""
+    import ctypes
+
+    from paper_2601_20499_b200 import _lib, errors
+    from paper_2601_20499_b200 import kernels as K
+
+    torch.manual_seed(11)
+    dev = torch.device("cuda:0")
+    width, hw, H, n_arenas = 64, 130, 70, 6
+    ctxs = [int(c) for c in torch.randint(1, 700, (H,))]
+    arenas = [K.KVArena(sum(K.KVArena.region_rows(c) for c in ctxs), width, dev) for _ in range(n_arenas)]
+    for a in arenas:
+        a.k.normal_()
+        a.v.normal_()
+    q = torch.randn(H * hw, width, device=dev).to(torch.bfloat16)
+    out = torch.full((H * hw, width), float("nan"), device=dev, dtype=torch.bfloat16)
+    work = []
+    for h, c in enumerate(ctxs):
+        a = arenas[(h // 3) % n_arenas]  # runs of 3 heads per arena: a launch may not exceed 4 arenas
+        work.append(K.HeadWork(a, a.allocate(c), c, h, h))
+    launches = K.prepare_attention(q, out, work, hw, 1 / math.sqrt(width))
+    assert len(launches) >= 3  # 70 heads > 64, and 4-arena runs of 12 heads
+    for launch in launches:
+        launch.launch()
+    torch.cuda.synchronize()
+    assert not torch.isnan(out.float()).any()
+    for h in (0, 13, 40, 64, 69):
+        w = work[h]
+        ref = _ref(q[h * hw:(h + 1) * hw], w.arena.k[w.base_row:w.base_row + w.n_tok],
+                   w.arena.v[w.base_row:w.base_row + w.n_tok], 1 / math.sqrt(width))
+        assert float((out[h * hw:(h + 1) * hw].float() - ref).abs().max() / ref.abs().max()) <= 2e-2, h
+    # the C ABI: num_heads beyond DF_MAX_HEADS is a shape error, not an out-of-bounds read
+    args = launches[0].keep[0]
+    saved = args.num_heads
+    args.num_heads = _lib.DF_MAX_HEADS + 1
+    try:
+        with pytest.raises(errors.ShapeError):
+            _lib.call("df_attn_fwd", ctypes.byref(args), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    finally:
+        args.num_heads = saved
