@@ -19,6 +19,7 @@ FIELDS = [
     "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
     "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "l1tex__m_xbar2l1tex_read_bytes.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
 ]
 STALLS = ["stall_long_sb", "stall_wait", "stall_barrier", "stall_selected", "stall_branch_resolving",
           "stall_short_sb", "stall_no_inst", "stall_not_selected", "stall_math", "stall_mio", "stall_dispatch"]
