@@ -154,8 +154,11 @@ DF_API int df_kv_arena_maps(const void* k_base, const void* v_base, int64_t rows
 DF_API int df_kv_append(const df_copy_seg* segs, int32_t n_segs, void* stream);
 /* Same copy, launched with programmatic stream serialization: if the kernel
  * before it on the stream is df_attn_fwd, it may start while that launch's last
- * wave is still running.  Only for destinations the preceding df_attn_fwd does
- * not read (e.g. the next layer's ring slots); the Python layer checks this. */
+ * wave is still running.  Only when the copy writes no byte the preceding
+ * df_attn_fwd reads or writes (Q, the K/V rows up to each head's last 128-row
+ * tile, out, probe buffers, workspace) and reads none it writes, e.g. the next
+ * layer's ring slots; the caller checks this (the Python layer compares merged
+ * byte ranges at launch time, kernels.PreparedLaunch). */
 DF_API int df_kv_append_overlapped(const df_copy_seg* segs, int32_t n_segs, void* stream);
 /* Bulk compaction: segment list already in device memory; chunk_prefix is a
  * device int64 [n_segs+1] exclusive prefix of per-segment 16-byte-chunk
