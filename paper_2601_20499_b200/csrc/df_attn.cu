@@ -14,7 +14,7 @@
 //
 // CTA = 12 warps (384 threads, 1 CTA/SM):
 //   warp 0      TMA producer (Q once; K and V rings)
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warp 1      TMEM allocator + tcgen05.mma issuer (warp-wide loop, elected lane issues)
 //   warps 2-3   idle (warpgroup 0 gives its registers to the softmax groups)
 //   warps 4-7   softmax / correction / epilogue for query tile 0 (rows 0-127)
 //   warps 8-11  same for query tile 1 (rows 128-255)
@@ -23,7 +23,7 @@
 // operand (from TMEM) of O += P V.  MMA issue order per kv tile j:
 //   S0_j = Q0 K_j^T | O1 += P1_{j-1} V_{j-1} | S1_j = Q1 K_j^T | O0 += P0_j V_j
 // so the tensor pipe always has a GEMM queued while either softmax group works.
-// Online softmax in the log2 domain with lazy rescaling (threshold 2^8).
+// Online softmax in the log2 domain with lazy rescaling (threshold 2^DF_RESCALE_THRESHOLD = 2^16).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
