@@ -175,7 +175,7 @@ DF_API int df_kv_pack_plan(const df_copy_seg* segs_host, int32_t n_segs,
  * order).  F is device double [num_heads][3]. */
 DF_API int df_scores_finalize(const float* probe_rows, const uint8_t* row_sampled,
                        int32_t num_heads, int32_t hw, double* F, void* stream);
-/* Host.  classes_out: 0 sink, 1 neighbor, 2 dummy (head_programming.py:254). */
+/* Host.  classes_out: 0 sink, 1 neighbor, 2 dummy (head_programming.py:38, _CLASS_CODES). */
 DF_API int df_greedy_classify(const double* F, int64_t total_heads, int64_t n_dummy,
                        int8_t* classes_out, double* objective_out);
 

@@ -12,7 +12,7 @@ from dataclasses import dataclass, field, replace
 
 import numpy as np
 
-SINK, NEIGHBOR, DUMMY = 0, 1, 2  # head_programming.py:254 code order
+SINK, NEIGHBOR, DUMMY = 0, 1, 2  # head_programming.py:38 (_CLASS_CODES order)
 CLASS_NAMES = ("sink", "neighbor", "dummy")
 
 # --------------------------------------------------------------------- rng
