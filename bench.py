@@ -247,19 +247,21 @@ def build_caches(df, cfg, dev, gen):
     return caches, arena
 
 
-def run_layers(df, cfg, caches, inputs, classes, mode, timed=True):
+def run_layers(df, cfg, caches, inputs, classes, mode, timed=True, chain=None):
     """One step (30 layers) through the public step functions.  ``timed``: True = CUDA events around
     every launch, False = none, an int = only that layer (per-launch events between a layer's FMHA and
-    the next layer's staging copy break their programmatic-dependent-launch pairing)."""
+    the next layer's staging copy break their programmatic-dependent-launch pairing).  ``chain``: a
+    kernels.LaunchChain -- this loop issues nothing but library launches on the stream, so each
+    layer's staging copy may overlap the previous layer's FMHA."""
     lcs = []
     for layer in range(L):
         q, k, v = inputs[layer]
         blocks = [df.FrameBlock(W, k[h], v[h]) for h in range(H)]
         t = timed if isinstance(timed, bool) else (layer == timed)
         if mode == "baseline":
-            out, lc = df.baseline_step(q, caches[layer], blocks, cfg, timed=t)
+            out, lc = df.baseline_step(q, caches[layer], blocks, cfg, timed=t, chain=chain)
         else:
-            out, lc = df.packed_step(q, caches[layer], blocks, classes, cfg, timed=t)
+            out, lc = df.packed_step(q, caches[layer], blocks, classes, cfg, timed=t, chain=chain)
         lcs.append(lc)
     return lcs
 
@@ -487,6 +489,8 @@ def batched_streams(df, cfg, dev, gen, packed, inputs, classes, args, B=4):
     rings and inputs, every layer's B requests in ONE FMHA launch through the public batched_step."""
     import torch
 
+    from paper_2601_20499_b200 import kernels as K
+
     caches_b, inputs_b = [packed], [inputs]
     pols = [df.derive_policy(df.HeadClass(ASSIGN[i % H]), cfg) for i in range(L * H)]
     for b in range(1, B):
@@ -501,6 +505,8 @@ def batched_streams(df, cfg, dev, gen, packed, inputs, classes, args, B=4):
     # batched_step then launches on it without a gather copy
     q_all = [torch.stack([inputs_b[b][layer][0] for b in range(B)]) for layer in range(L)]
 
+    chain = K.LaunchChain()
+
     def step():
         for layer in range(L):
             reqs = []
@@ -509,7 +515,7 @@ def batched_streams(df, cfg, dev, gen, packed, inputs, classes, args, B=4):
                 q = q_all[layer][b]
                 reqs.append(df.StepRequest("packed", q, caches_b[b][layer],
                                            [df.FrameBlock(W, k[h], v[h]) for h in range(H)], classes))
-            df.batched_step(reqs, cfg, timed=False)
+            df.batched_step(reqs, cfg, timed=False, chain=chain)
         return []
 
     t, _ = time_steps(step, max(3, args.steps // 2), args.warmup)
@@ -675,6 +681,7 @@ def gpu_arm(args, ws, rank, local):
 
     import paper_2601_20499_b200 as df
     from paper_2601_20499_b200 import _lib
+    from paper_2601_20499_b200 import kernels as K
 
     dev = torch.device("cuda", local)
     _lib.require_device(local)
@@ -689,8 +696,9 @@ def gpu_arm(args, ws, rank, local):
 
     # all-context comparator (same kernel, every head baseline-window)
     barrier(ws)
-    t_base, _ = time_steps(lambda: run_layers(df, cfg, caches, inputs, None, "baseline", timed=False), args.steps,
-                           args.warmup)
+    chain = K.LaunchChain()
+    t_base, _ = time_steps(lambda: run_layers(df, cfg, caches, inputs, None, "baseline", timed=False, chain=chain),
+                           args.steps, args.warmup)
 
     # classification-time context packing: one df_kv_pack launch for all 360 heads
     flat = [c for layer in caches for c in layer]
@@ -717,8 +725,9 @@ def gpu_arm(args, ws, rank, local):
         # roofline's launch duration; the other layers carry no per-launch events, which would sit
         # between a layer's FMHA and the next layer's staging copy and break their programmatic-
         # dependent-launch pairing (the copy fills the FMHA's last wave)
-        t_step, lcs = time_steps(lambda: run_layers(df, cfg, packed, inputs, classes, "packed", timed=L // 2),
-                                 args.steps, args.warmup)
+        chain = K.LaunchChain()
+        t_step, lcs = time_steps(lambda: run_layers(df, cfg, packed, inputs, classes, "packed", timed=L // 2,
+                                                    chain=chain), args.steps, args.warmup)
     t_step = barrier_max(t_step, ws)
     attn_ns = [step[L // 2].attn_time_ns for step in lcs]
 

@@ -153,15 +153,19 @@ class OutputTarget:
 
 def _dispatch(q_heads, caches: list[HeadKVCache], current_blocks: list[FrameBlock], head_dim: int,
               groups: list[list[int]], probe: ProbeRequest | None = None, stream=None, timed: bool = True,
-              target: OutputTarget | None = None):
+              target: OutputTarget | None = None, chain: K.LaunchChain | None = None,
+              workspace: K.Workspace | None = None):
     """Stage current frames, check the logical groups, launch one ragged FMHA."""
     if stream is not None:
         with torch.cuda.stream(stream):
-            return _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, stream, timed, target)
-    return _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, None, timed, target)
+            return _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, stream, timed, target,
+                                chain, workspace)
+    return _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, None, timed, target, chain,
+                        workspace)
 
 
-def _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, stream, timed, target=None):
+def _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, stream, timed, target=None, chain=None,
+                 workspace=None):
     H = len(caches)
     if len(current_blocks) != H:
         raise ShapeError(f"{len(current_blocks)} current blocks for {H} caches")
@@ -212,20 +216,20 @@ def _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, strea
                             probe.probe_rows)
     lc = LayerCounters(kernel_calls=calls, key_token_macs=macs, physical_launches=0)
     s = stream if stream is not None else torch.cuda.current_stream(device)
-    # build every launch first so the timed region holds no host work.  The staging copy may
-    # overlap the previous FMHA launch on this stream (programmatic dependent launch) when the
-    # two touch disjoint bytes -- checked when the copy launches (kernels.PreparedLaunch)
-    copies = K.prepare_copies([sg[:6] for sg in segs], overlapped=not timed)
-    attn = K.prepare_attention(q2, out, work, hw, 1.0 / math.sqrt(head_dim), pb, None, s, peers)
+    # build every launch first so the timed region holds no host work.  Inside a caller's
+    # LaunchChain the staging copy may overlap the previous FMHA of the chain (programmatic
+    # dependent launch) when the two touch disjoint bytes -- checked when the copy launches
+    copies = K.prepare_copies([sg[:6] for sg in segs], overlapped=chain is not None)
+    attn = K.prepare_attention(q2, out, work, hw, 1.0 / math.sqrt(head_dim), pb, None, s, peers, workspace)
     if timed:
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record(s)
     for launch in copies:
-        launch.launch(s)
+        launch.launch(s, chain)
     if timed:
         ev[1].record(s)
     for launch in attn:
-        launch.launch(s)
+        launch.launch(s, chain)
     if timed:
         ev[2].record(s)
         lc._events = tuple(ev)
@@ -239,13 +243,21 @@ def _dispatch_on(q_heads, caches, current_blocks, head_dim, groups, probe, strea
 
 def baseline_step(q_heads, caches: list[HeadKVCache], current_blocks: list[FrameBlock], config: SessionConfig,
                   *, stream=None, probe: ProbeRequest | None = None, timed: bool = True,
-                  target: OutputTarget | None = None):
-    """Full-window attention for every head of one layer (engine.py:140-152)."""
+                  target: OutputTarget | None = None, chain: K.LaunchChain | None = None,
+                  workspace: K.Workspace | None = None):
+    """Full-window attention for every head of one layer (engine.py:140-152).
+
+    Keyword extensions of the reference signature: ``stream``; ``probe`` (fused DHP epilogue);
+    ``timed`` (CUDA events -> LayerCounters.wall_time_ns); ``target`` (head-parallel output
+    buffer); ``chain`` (kernels.LaunchChain: the caller issues its steps back to back on one
+    stream, so the staging copy may overlap the previous FMHA); ``workspace`` (split-KV
+    workspace, default the caches' arena's).
+    """
     for c in caches:
         if c.policy.kind != "baseline_window":
             raise ConfigError(f"baseline_step got a {c.policy.kind} cache")
     return _dispatch(q_heads, caches, current_blocks, config.head_dim, [list(range(len(caches)))], probe, stream,
-                     timed, target)
+                     timed, target, chain, workspace)
 
 
 def _class_groups(classes: list[HeadClass]) -> list[list[int]]:
@@ -253,16 +265,18 @@ def _class_groups(classes: list[HeadClass]) -> list[list[int]]:
 
 
 def hma_step(q_heads, caches, current_blocks, classes: list[HeadClass], config: SessionConfig, *, stream=None,
-             probe: ProbeRequest | None = None, timed: bool = True, target: OutputTarget | None = None):
+             probe: ProbeRequest | None = None, timed: bool = True, target: OutputTarget | None = None,
+             chain: K.LaunchChain | None = None, workspace: K.Workspace | None = None):
     """Class-specific contexts; logically one call per class present (engine.py:161-174)."""
     if len(classes) != len(caches):
         raise AssignmentError(f"{len(classes)} classes for {len(caches)} heads in this layer")
     return _dispatch(q_heads, caches, current_blocks, config.head_dim, _class_groups(list(classes)), probe, stream,
-                     timed, target)
+                     timed, target, chain, workspace)
 
 
 def packed_step(q_heads, caches, current_blocks, classes: list[HeadClass], config: SessionConfig, *, stream=None,
-                probe: ProbeRequest | None = None, timed: bool = True, target: OutputTarget | None = None):
+                probe: ProbeRequest | None = None, timed: bool = True, target: OutputTarget | None = None,
+                chain: K.LaunchChain | None = None, workspace: K.Workspace | None = None):
     """Dummy+sink share one logical call, neighbors the other (engine.py:177-195)."""
     if not config.packing_enabled:
         raise ConfigError("packed_step requires packing_enabled")
@@ -270,7 +284,8 @@ def packed_step(q_heads, caches, current_blocks, classes: list[HeadClass], confi
         raise AssignmentError(f"{len(classes)} classes for {len(caches)} heads in this layer")
     ds = [h for h, c in enumerate(classes) if c is not HeadClass.NEIGHBOR]
     nb = [h for h, c in enumerate(classes) if c is HeadClass.NEIGHBOR]
-    return _dispatch(q_heads, caches, current_blocks, config.head_dim, [ds, nb], probe, stream, timed, target)
+    return _dispatch(q_heads, caches, current_blocks, config.head_dim, [ds, nb], probe, stream, timed, target, chain,
+                     workspace)
 
 
 @dataclass
@@ -320,7 +335,8 @@ def _adjacent_rows(qs: list[torch.Tensor]) -> torch.Tensor | None:
     return q0.as_strided((rows, q0.shape[1]), (q0.shape[1], 1))
 
 
-def batched_step(requests: Sequence[StepRequest], config: SessionConfig, *, stream=None, timed: bool = True):
+def batched_step(requests: Sequence[StepRequest], config: SessionConfig, *, stream=None, timed: bool = True,
+                 chain: K.LaunchChain | None = None, workspace: K.Workspace | None = None):
     """Several independent sessions' layers (SURVEY 8(e) / BASELINE configs[4]: a batch of video streams
     on one GPU) in ONE ragged FMHA launch (more launches only past DF_MAX_HEADS heads or DF_MAX_ARENAS
     arenas).  Each request keeps its own logical calls, MAC counters and errors; the batch fills the
@@ -375,17 +391,17 @@ def batched_step(requests: Sequence[StepRequest], config: SessionConfig, *, stre
         if q2 is None:  # requests' Q not laid out back to back in one allocation: gather them
             q2 = torch.cat(qs, 0)
         out = torch.empty(base * hw, d8, dtype=torch.bfloat16, device=device)
-        copies = K.prepare_copies([sg[:6] for sg in segs], overlapped=not timed)
-        attn = K.prepare_attention(q2, out, work, hw, 1.0 / math.sqrt(d), None, None, s)
+        copies = K.prepare_copies([sg[:6] for sg in segs], overlapped=chain is not None)
+        attn = K.prepare_attention(q2, out, work, hw, 1.0 / math.sqrt(d), None, None, s, workspace=workspace)
         if timed:
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
             ev[0].record(s)
         for launch in copies:
-            launch.launch(s)
+            launch.launch(s, chain)
         if timed:
             ev[1].record(s)
         for launch in attn:
-            launch.launch(s)
+            launch.launch(s, chain)
         if timed:
             ev[2].record(s)
         del segs
@@ -921,6 +937,8 @@ class StepGraph:
         self.k = [torch.zeros(shape, dtype=torch.bfloat16, device=dev) for _ in caches]
         self.v = [torch.zeros(shape, dtype=torch.bfloat16, device=dev) for _ in caches]
         self.outputs: list[torch.Tensor] = []
+        # the graph's own split workspace (eager launches on the caches' arena never share its counters)
+        self.workspace = K.Workspace(dev)
         self.graph = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
@@ -933,14 +951,16 @@ class StepGraph:
 
     def _launch_all(self) -> list[torch.Tensor]:
         outs = []
+        chain = K.LaunchChain()  # every launch of the iteration is the library's own, back to back
+        kw = dict(timed=False, chain=chain, workspace=self.workspace)
         for layer, caches in enumerate(self.caches):
             blocks = [FrameBlock(self.frame_id, self.k[layer][h], self.v[layer][h]) for h in range(len(caches))]
             if self.mode == "baseline" or self.classes is None:
-                o, _ = baseline_step(self.q[layer], caches, blocks, self.config, timed=False)
+                o, _ = baseline_step(self.q[layer], caches, blocks, self.config, **kw)
             elif self.mode == "hma":
-                o, _ = hma_step(self.q[layer], caches, blocks, self.classes[layer], self.config, timed=False)
+                o, _ = hma_step(self.q[layer], caches, blocks, self.classes[layer], self.config, **kw)
             else:
-                o, _ = packed_step(self.q[layer], caches, blocks, self.classes[layer], self.config, timed=False)
+                o, _ = packed_step(self.q[layer], caches, blocks, self.classes[layer], self.config, **kw)
             outs.append(o)
         return outs
 

@@ -42,6 +42,33 @@ def _stream_handle(stream: torch.cuda.Stream | None) -> ctypes.c_void_p:
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+class Workspace:
+    """Split-KV workspace of df_attn_fwd (piece partials + combine counters), owned by its user.
+
+    Zero-filled at allocation; the kernel returns every combine counter to
+    zero, so the next launch reuses it without a memset.  Launches that share
+    one workspace must be stream-ordered: each KVArena (one per session) and
+    each captured graph owns its own, so independent sessions on different
+    streams never share counters.  Growing keeps the old buffer alive, since a
+    captured CUDA graph may still launch into it.
+    """
+
+    def __init__(self, device: torch.device | str):
+        self.device = torch.device(device)
+        self.buf: torch.Tensor | None = None
+        self._retired: list[torch.Tensor] = []
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes:
+            if torch.cuda.is_current_stream_capturing():
+                raise ShapeError(f"split workspace must grow to {nbytes} B during CUDA-graph capture; "
+                                 "run the captured launches once eagerly first")
+            if self.buf is not None:
+                self._retired.append(self.buf)
+            self.buf = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
 class KVArena:
     """One device allocation holding the K and V rings of many heads.
 
@@ -75,6 +102,7 @@ class KVArena:
         )
         self.maps = bytes(buf)
         self._next = 0
+        self.workspace = Workspace(self.device)
 
     def allocate(self, tokens: int) -> int:
         """Reserve a region of ``tokens`` rows; returns its first row."""
@@ -136,8 +164,35 @@ def _hits(merged: tuple[list[int], list[int]], ranges: list[tuple[int, int]]) ->
     return False
 
 
-# byte footprint of the last df_attn_fwd launched on each stream: (touched, written), merged
-_LAST_FMHA: dict[int, tuple[tuple[list[int], list[int]], tuple[list[int], list[int]]]] = {}
+class LaunchChain:
+    """Library launches that one caller issues back to back on one stream.
+
+    The staging copy of a layer may run as ``df_kv_append_overlapped``
+    (programmatic dependent launch: it starts on the SMs the previous FMHA's
+    last wave leaves idle) only inside a chain: the caller that owns the chain
+    promises that no kernel outside the library runs on the stream between its
+    chained launches (a foreign producer that triggers its dependents early
+    could otherwise let the copy read unfinished data).  StepGraph, the
+    benchmark's step loops and batched streams hold chains; the public step
+    functions without ``chain=`` always emit the plain, fully serialised copy.
+
+    State is per chain object: the footprint of the last FMHA launched through
+    it, on which stream.  A copy overlaps only when that FMHA touches none of
+    the bytes the copy writes and writes none it reads.
+    """
+
+    __slots__ = ("_stream", "_touched", "_written")
+
+    def __init__(self):
+        self.reset()
+
+    def reset(self) -> None:
+        self._stream = None
+        self._touched = self._written = None
+
+    def _may_overlap(self, stream: int, reads, writes) -> bool:
+        return (self._touched is not None and self._stream == stream and not _hits(self._touched, writes)
+                and not _hits(self._written, reads))
 
 
 class PreparedLaunch:
@@ -145,10 +200,9 @@ class PreparedLaunch:
 
     ``touched`` / ``written`` (df_attn_fwd): the byte ranges the launch reads or writes / writes.
     ``reads`` / ``writes`` (a df_kv_append_overlapped candidate): the copy's source and
-    destination ranges.  The overlapped variant may start while the previous df_attn_fwd on the
-    stream still runs, so it is used only when, at launch time, that FMHA's footprint is
-    disjoint from what the copy writes and its writes are disjoint from what the copy reads;
-    otherwise the plain, fully serialised df_kv_append runs.
+    destination ranges.  The overlapped variant is used only through a :class:`LaunchChain`
+    whose last FMHA is disjoint from the copy; otherwise the plain df_kv_append runs.
+    ``last_fn``: the entry point the most recent ``launch`` called.
     """
 
     def __init__(self, fn: str, args: tuple, keep: tuple, touched=None, written=None, reads=None, writes=None):
@@ -156,16 +210,20 @@ class PreparedLaunch:
         self.touched = _merge(touched) if touched is not None else None
         self.written = _merge(written) if written is not None else None
         self.reads, self.writes = reads, writes
+        self.last_fn = None
 
-    def launch(self, stream: torch.cuda.Stream | None = None) -> None:
+    def launch(self, stream: torch.cuda.Stream | None = None, chain: LaunchChain | None = None) -> None:
         h = _stream_handle(stream)
         fn = self.fn
         if self.writes is not None:
-            last = _LAST_FMHA.get(h.value or 0)
-            if last is None or _hits(last[0], self.writes) or _hits(last[1], self.reads):
+            if chain is None or not chain._may_overlap(h.value or 0, self.reads, self.writes):
                 fn = "df_kv_append"
-        elif self.touched is not None:
-            _LAST_FMHA[h.value or 0] = (self.touched, self.written)
+        elif chain is not None:
+            if self.touched is not None:
+                chain._stream, chain._touched, chain._written = h.value or 0, self.touched, self.written
+            elif fn != "df_kv_append":
+                chain.reset()
+        self.last_fn = fn
         _lib.call(fn, *self.args, h)
 
 
@@ -179,6 +237,7 @@ def prepare_attention(
     pair: bool | None = None,
     stream: torch.cuda.Stream | None = None,
     peer_out: Sequence[int] | None = None,
+    workspace: "Workspace | None" = None,
 ) -> list[PreparedLaunch]:
     """Build the launch(es) of one ragged attention over every head in ``work``.
 
@@ -188,6 +247,9 @@ def prepare_attention(
     contiguous runs (a session uses one arena: one launch).  ``peer_out``:
     device pointers of buffers laid out like ``out`` (other ranks' gathered
     outputs) that receive the same rows -- the fused head-output all-gather.
+    ``workspace``: split-KV partials + combine counters; default: the first
+    head's arena's (one session = one arena = one writer, so launches sharing it
+    are stream-ordered).
     """
     if not work:
         return []
@@ -207,7 +269,8 @@ def prepare_attention(
             sub_probe = None
             if probe is not None:
                 sub_probe = ProbeBuffers(probe.region_of_slot[sl], probe.row_sampled, probe.probe_rows[sl])
-            out_launches += prepare_attention(q, out, work[sl], hw, scale, sub_probe, pair, stream, peer_out)
+            out_launches += prepare_attention(q, out, work[sl], hw, scale, sub_probe, pair, stream, peer_out,
+                                              workspace)
         return out_launches
     if q.dtype != torch.bfloat16 or out.dtype != torch.bfloat16:
         raise ShapeError("q and out must be bfloat16")
@@ -268,7 +331,9 @@ def prepare_attention(
     _lib.call("df_attn_workspace_bytes", ctypes.byref(args), ctypes.byref(need))
     ws = None
     if need.value > 0:
-        ws = _split_workspace(q.device, _stream_handle(stream).value, need.value)
+        if workspace is None:
+            workspace = work[0].arena.workspace
+        ws = workspace.get(need.value)
         args.workspace = ws.data_ptr()
         args.workspace_bytes = ws.numel()
     written = [_span(out)]
@@ -305,40 +370,20 @@ def attention(
     probe: ProbeBuffers | None = None,
     stream: torch.cuda.Stream | None = None,
     pair: bool | None = None,
+    workspace: "Workspace | None" = None,
+    chain: LaunchChain | None = None,
 ) -> None:
     """Ragged attention over every head in ``work`` (see prepare_attention)."""
-    for launch in prepare_attention(q, out, work, hw, scale, probe, pair, stream):
-        launch.launch(stream)
-
-
-_WORKSPACES: dict[tuple[int, int], torch.Tensor] = {}
-_RETIRED_WORKSPACES: list[torch.Tensor] = []
-
-
-def _split_workspace(device: torch.device, stream_handle: int, nbytes: int) -> torch.Tensor:
-    """Per-(device, stream) stream-K workspace (split partials + combine counters).
-
-    Zero-filled at allocation; the kernel returns every combine counter to
-    zero, so the next launch on the same stream reuses it without a memset.
-    """
-    key = (device.index if device.index is not None else torch.cuda.current_device(), stream_handle or 0)
-    ws = _WORKSPACES.get(key)
-    if ws is None or ws.numel() < nbytes:
-        if ws is not None:
-            # a captured CUDA graph (StepGraph, Session(graphs=True)) may still launch into the old
-            # buffer: keep it alive instead of returning it to the allocator
-            _RETIRED_WORKSPACES.append(ws)
-        ws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
-        _WORKSPACES[key] = ws
-    return ws
+    for launch in prepare_attention(q, out, work, hw, scale, probe, pair, stream, workspace=workspace):
+        launch.launch(stream, chain)
 
 
 def prepare_copies(segs: list[tuple[int, int, int, int, int, int]], overlapped: bool = False) -> list[PreparedLaunch]:
     """df_kv_append launches (<= DF_MAX_APPEND_SEGS segments each), built ahead of time.
 
-    ``overlapped``: the first launch may start during the previous df_attn_fwd on the stream
-    (df_kv_append_overlapped); PreparedLaunch.launch checks, at launch time, that the two do not
-    touch the same bytes and falls back to the serialised df_kv_append when they might.
+    ``overlapped``: the first launch is a df_kv_append_overlapped candidate; launched through a
+    LaunchChain whose last FMHA touches none of its bytes it may start during that FMHA, otherwise
+    (no chain, or a possible overlap) it runs as the serialised df_kv_append.
     """
     out = []
     for i in range(0, len(segs), _lib.DF_MAX_APPEND_SEGS):

@@ -113,13 +113,13 @@ class HeadParallelSession(Session):
         return head_partition(self.config.num_heads, self.world, self.rank)
 
     def _gather_outputs(self, layer: int, outputs: torch.Tensor) -> torch.Tensor:
-        if self.fused is not None and outputs.data_ptr() == self.fused.buffer(layer).data_ptr():
+        if self.fused is not None and outputs.data_ptr() == self.fused.current().data_ptr():
             # every rank's FMHA epilogue stored its heads' rows into all buffers
             if self.stream is not None:
                 with torch.cuda.stream(self.stream):
-                    self.fused.barrier(layer)
+                    self.fused.barrier()
             else:
-                self.fused.barrier(layer)
+                self.fused.barrier()
             return outputs[:, :, : self.config.head_dim]
         if self.owners is not None:
             return gather_head_outputs_owned(outputs, self.owners[layer], self.group)
@@ -286,13 +286,18 @@ class FusedHeadGather:
 
     Two bf16 [total_heads * HW, d8] buffers per rank in symmetric memory
     (torch.distributed._symmetric_memory: the allocation and the mapping of
-    every rank's buffer into every process), alternating by layer.  The FMHA
+    every rank's buffer into every process), used in turns.  The FMHA
     epilogue of each rank stores its heads' rows into its own buffer and, over
     NVLink, into the peers' (df_attn_args.peer_out), so the gather overlaps the
-    attention tile by tile and no NCCL all-gather runs.  ``barrier(layer)``
-    (a device-side signal/wait on the stream) orders the peers' stores before
-    this rank reads the buffer; alternating buffers keep layer l+1's stores
-    off the buffer a slower rank may still be reading for layer l.
+    attention tile by tile and no NCCL all-gather runs.  ``barrier()`` (a
+    device-side signal/wait on the stream) orders the peers' stores before
+    this rank reads the buffer, then passes the turn to the other buffer: the
+    next fused gather's stores go to the buffer a slower rank is not reading.
+    The turn advances once per fused gather (not by layer index), so it
+    alternates across the end of a denoise iteration whatever the layer count
+    (with an odd count, layer L-1 and the next iteration's layer 0 would
+    otherwise share a buffer).  Every rank runs the same sequence of fused
+    gathers, so the turns agree.
     """
 
     def __init__(self, rows: int, width: int, group, device):
@@ -311,14 +316,18 @@ class FusedHeadGather:
             self.bufs.append(t)
             self.handles.append(h)
             self.peers.append([view(r) for r in range(h.world_size) if r != h.rank])
+        self.turn = 0
 
-    def buffer(self, layer: int) -> torch.Tensor:
-        return self.bufs[layer % 2]
+    def current(self) -> torch.Tensor:
+        """The buffer the next (or pending) fused gather writes."""
+        return self.bufs[self.turn % 2]
 
     def target(self, layer: int, heads):
         from .engine import OutputTarget
 
-        return OutputTarget(self.bufs[layer % 2], list(heads), self.peers[layer % 2])
+        i = self.turn % 2
+        return OutputTarget(self.bufs[i], list(heads), self.peers[i])
 
-    def barrier(self, layer: int) -> None:
-        self.handles[layer % 2].barrier(channel=0)
+    def barrier(self) -> None:
+        self.handles[self.turn % 2].barrier(channel=0)
+        self.turn += 1

@@ -430,12 +430,13 @@ for layer in range(L):
     layers.append((caches, rnd(H, HW, d), [df.FrameBlock(W, rnd(HW, d), rnd(HW, d)) for _ in range(H)]))
 names.clear()  # the cache set-up above stages frames with plain copies
 outs = []
+chain = K.LaunchChain()  # this loop issues only library launches on the stream
 for rep in range(3):  # several passes: layer 0 of a pass follows layer L-1 (disjoint rings, overlapped copy)
     for caches, q, blocks in layers:
-        o, _ = df.packed_step(q, caches, blocks, classes, cfg, timed=False)
+        o, _ = df.packed_step(q, caches, blocks, classes, cfg, timed=False, chain=chain)
         outs.append(o)
     # the same layer twice in a row: its pending slots are rewritten, so this copy must not overlap
-    o, _ = df.packed_step(layers[0][1], layers[0][0], layers[0][2], classes, cfg, timed=False)
+    o, _ = df.packed_step(layers[0][1], layers[0][0], layers[0][2], classes, cfg, timed=False, chain=chain)
     outs.append(o)
 # an FMHA launched straight through kernels.attention over layer 1's rings, then layer 1's step:
 # its staging copy rewrites rows that FMHA reads, so it must not overlap it
@@ -443,9 +444,23 @@ caches1, q1, blocks1 = layers[1]
 junk = torch.empty(H * HW, d, dtype=torch.bfloat16, device=dev)
 K.attention(q1.reshape(H * HW, d).contiguous(), junk,
             [K.HeadWork(c.storage.arena, c.storage.base_row, c.storage.slots * HW, h, h) for h, c in enumerate(caches1)],
-            HW, 1.0 / math.sqrt(d))
-o, _ = df.packed_step(q1, caches1, blocks1, classes, cfg, timed=False)
+            HW, 1.0 / math.sqrt(d), chain=chain)
+o, _ = df.packed_step(q1, caches1, blocks1, classes, cfg, timed=False, chain=chain)
 outs.append(o)
+# a foreign producer between an FMHA and the next step, outside any chain (the public default):
+# a torch matmul writes the current frame's K/V right before the step that stages them
+caches2, q2, blocks2 = layers[2]
+wk = torch.randn(d, d, device=dev, generator=g).to(torch.bfloat16) / d ** 0.5
+src = [(rnd(HW, d), rnd(HW, d)) for _ in blocks2]
+for rep in range(4):
+    df.packed_step(q1, caches1, blocks1, classes, cfg, timed=False)
+    for b, (ks, vs) in zip(blocks2, src):
+        torch.matmul(ks, wk, out=b.keys)
+        torch.matmul(vs, wk, out=b.values)
+        ks.mul_(1.5)
+        vs.mul_(1.5)
+    o, _ = df.packed_step(q2, caches2, blocks2, classes, cfg, timed=False)
+    outs.append(o)
 torch.cuda.synchronize()
 torch.save(([o.cpu() for o in outs], [n for n in names if n.startswith("df_kv_append")]), sys.argv[2])
 """
@@ -456,9 +471,11 @@ L_PDL = 12
 
 def test_overlapped_staging_copy_matches_serialized(tmp_path):
     """Programmatic dependent launch of the staging copy (df_kv_append_overlapped after an FMHA
-    that reads other rings): every output of a 12-layer x 3-pass loop with split-KV plans is
-    bitwise equal to the fully serialized run (DF_APPEND_PDL=0), including the same layer twice in
-    a row (which must not overlap) -- no race on the rings, the outputs or the shared workspace."""
+    that reads other rings, inside a LaunchChain): every output of a 12-layer x 3-pass loop with
+    split-KV plans is bitwise equal to the fully serialized run (DF_APPEND_PDL=0), including the same
+    layer twice in a row (which must not overlap) -- no race on the rings, the outputs or the shared
+    workspace.  A torch matmul producing K/V between an FMHA and the next public step (no chain)
+    gets the plain copy and the same outputs."""
     import subprocess
     import sys as _sys
 
@@ -471,10 +488,11 @@ def test_overlapped_staging_copy_matches_serialized(tmp_path):
                        env=dict(os.environ, DF_APPEND_PDL=v))
         res[v] = torch.load(tmp_path / f"o{v}.pt")
     (o1, copies), (o0, _) = res["1"], res["0"]
-    assert len(o1) == len(o0) == 40
+    assert len(o1) == len(o0) == 44
     for a, b in zip(o1, o0):
         assert torch.equal(a, b)
     # per pass: layer 0 follows no FMHA or the repeat of layer 0 (plain), layers 1..11 and the repeat
-    # (after layer 11) overlap; the step after the direct FMHA over its own rings is plain
+    # (after layer 11) overlap; the step after the direct FMHA over its own rings is plain; steps
+    # outside a chain (after the foreign producer) are always plain
     plain, over = "df_kv_append", "df_kv_append_overlapped"
-    assert copies == ([plain] + [over] * L_PDL) * 3 + [plain]
+    assert copies == ([plain] + [over] * L_PDL) * 3 + [plain] + [plain] * 8

@@ -261,33 +261,39 @@ def test_batched_step_request_checks_on_host():
         df.batched_step([], cfg)
 
 
-def test_overlapped_copy_falls_back_when_the_last_fmha_touches_its_bytes(monkeypatch):
-    """df_kv_append_overlapped (programmatic dependent launch) runs only when the previous
-    df_attn_fwd on the stream touches none of the bytes the copy writes and writes none it reads."""
+def test_overlapped_copy_only_inside_a_chain_and_when_disjoint(monkeypatch):
+    """df_kv_append_overlapped (programmatic dependent launch) runs only through a LaunchChain whose
+    last df_attn_fwd on the same stream touches none of the bytes the copy writes and writes none
+    it reads; without a chain (the public default) the copy is always the serialised df_kv_append."""
     from paper_2601_20499_b200 import kernels as K
 
     calls = []
     monkeypatch.setattr(_lib, "call", lambda fn, *a: calls.append(fn))
 
     class _S:
-        cuda_stream = 0x5EED
+        def __init__(self, h):
+            self.cuda_stream = h
 
-    s = _S()
-    K._LAST_FMHA.pop(s.cuda_stream, None)
+    s, s2 = _S(0x5EED), _S(0x5EEE)
     fmha = K.PreparedLaunch("df_attn_fwd", (), (), touched=[(1000, 2000), (5000, 6000)], written=[(5000, 6000)])
+    other = K.PreparedLaunch("df_out_project", (), ())
 
     def copy(src, dst, rows=4, ld=64, nbytes=64):
         return K.prepare_copies([(src, dst, rows, ld, ld, nbytes)], overlapped=True)[0]
 
-    copy(10_000, 20_000).launch(s)  # no FMHA launched on this stream yet
-    fmha.launch(s)
-    copy(10_000, 20_000).launch(s)  # disjoint
-    copy(10_000, 1900).launch(s)  # writes into bytes the FMHA reads
-    copy(5900, 20_000).launch(s)  # reads bytes the FMHA writes
-    copy(1000, 20_000).launch(s)  # reads what the FMHA reads: fine
-    copy(10_000, 2000).launch(s)  # [2000, 2256): adjacent, disjoint
-    copy(10_000, 4800, rows=4, ld=64, nbytes=64).launch(s)  # [4800, 5056) overlaps [5000, 6000)
-    assert calls == ["df_kv_append", "df_attn_fwd", "df_kv_append_overlapped", "df_kv_append", "df_kv_append",
-                     "df_kv_append_overlapped", "df_kv_append_overlapped", "df_kv_append"]
+    chain = K.LaunchChain()
+    copy(10_000, 20_000).launch(s, chain)  # no FMHA launched through the chain yet
+    fmha.launch(s, chain)
+    copy(10_000, 20_000).launch(s, chain)  # disjoint
+    copy(10_000, 20_000).launch(s)  # disjoint, but no chain: plain
+    copy(10_000, 20_000).launch(s2, chain)  # the chain's FMHA ran on another stream: plain
+    copy(10_000, 1900).launch(s, chain)  # writes into bytes the FMHA reads
+    copy(5900, 20_000).launch(s, chain)  # reads bytes the FMHA writes
+    copy(1000, 20_000).launch(s, chain)  # reads what the FMHA reads: fine
+    copy(10_000, 2000).launch(s, chain)  # [2000, 2256): adjacent, disjoint
+    copy(10_000, 4800, rows=4, ld=64, nbytes=64).launch(s, chain)  # [4800, 5056) overlaps [5000, 6000)
+    other.launch(s, chain)  # any other library launch ends the pairing
+    copy(10_000, 20_000).launch(s, chain)
+    p, o = "df_kv_append", "df_kv_append_overlapped"
+    assert calls == [p, "df_attn_fwd", o, p, p, p, p, o, o, p, "df_out_project", p]
     assert K._merge([(5, 9), (0, 3), (3, 4), (8, 12)]) == ([0, 5], [4, 12])
-    K._LAST_FMHA.pop(s.cuda_stream, None)
