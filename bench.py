@@ -743,7 +743,9 @@ def gpu_arm(args, ws, rank, local):
 
     fused = full_layer(df, cfg, packed, classes, dev, gen, args, ws, bf16_peak)
     extra = {}
-    if not args.no_configs:
+    if ws > 1:
+        extra = {"note": "per-GPU config timings are measured in the N=1 run"}
+    elif not args.no_configs:
         extra = kernel_configs(df, dev, bf16_peak)
         extra["rollout_c3"] = rollout_c3(df, dev)
         extra["streams4_batched_step_c5"] = batched_streams(df, cfg, dev, gen, packed, inputs, classes, args)
@@ -834,10 +836,35 @@ def gpu_arm(args, ws, rank, local):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
-    if rank == 0 and ws == 1 and not args.no_cpu:
+    if ws > 1:  # every rank's clocks during its timed region; the line's clocks are the slowest rank's
+        import torch.distributed as dist
+
+        per_rank = [None] * ws
+        dist.all_gather_object(per_rank, line["clocks"])
+        line["clocks_per_rank"] = per_rank
+        line["clocks"] = dict(min(per_rank, key=lambda c: c["sm_mhz"] or 0),
+                              reasons=sorted({r for c in per_rank for r in c["reasons"]}))
+    if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_sample(1)
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def spawn_command(args_argv: list[str], gpus: int, port: int) -> list[str]:
+    """torchrun command that re-launches this script with one rank per GPU (``--gpus N`` without a
+    launcher around it)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *args_argv]
+
+
+def _free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
 
 
 def main():
@@ -851,10 +878,24 @@ def main():
     ap.add_argument("--mode", default="streams", choices=["streams", "headpar"],
                     help="streams: independent streams per GPU (default, weak scaling); headpar: configs[3], one "
                          "high-resolution video with its heads sharded over the GPUs (strong scaling)")
+    ap.add_argument("--rank-check", action="store_true", help=argparse.SUPPRESS)  # test hook: report ranks, exit
     args = ap.parse_args()
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None and args.gpus > 1 and args.impl == "ours":
+        # one process per GPU: re-launch under torchrun (NCCL INIT lines on stderr let a reader count ranks)
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        sys.exit(subprocess.call(spawn_command(sys.argv[1:], args.gpus, _free_port()), env=env))
+    if ws_env is not None and int(ws_env) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}; launch one rank per GPU")
+    if args.rank_check:
+        print(json.dumps({"rank": int(os.environ.get("RANK", "0")), "world": int(ws_env or 1)}), flush=True)
+        return
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
-        reference_arm(args, int(os.environ.get("WORLD_SIZE", "1")), rank)
+        reference_arm(args, int(ws_env or "1"), rank)
         return
     ws, rank, local = dist_setup()
     if args.mode == "headpar":

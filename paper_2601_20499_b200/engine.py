@@ -673,7 +673,7 @@ class Session:
                 s.wait_stream(cs)
                 g = torch.cuda.CUDAGraph()
                 x_cap = type(x_in)(x_in.f32.clone(), x_in.bf16.clone())
-                with torch.cuda.graph(g, stream=cs, pool=self._graph_pool):
+                with torch.cuda.graph(g, stream=cs, pool=self._graph_pool, capture_error_mode="thread_local"):
                     self._layers(x_cap, ar_step, t, timed=False)
             finally:
                 self.stream = saved
@@ -945,7 +945,7 @@ class StepGraph:
         with torch.cuda.stream(side):
             self._launch_all()  # eager warm-up: allocates the stream's workspace, checks every error path
         torch.cuda.current_stream(dev).wait_stream(side)
-        with torch.cuda.graph(self.graph, stream=side):
+        with torch.cuda.graph(self.graph, stream=side, capture_error_mode="thread_local"):
             self.outputs = self._launch_all()
         self.kernel_launches = 2 * len(caches)
 

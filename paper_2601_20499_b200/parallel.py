@@ -45,12 +45,15 @@ def _all_gather(t: torch.Tensor, group) -> torch.Tensor:
     """Stack every rank's equally shaped tensor along a new leading dim."""
     world = dist.get_world_size(group)
     t = t.contiguous()
-    out = torch.empty((world, *t.shape), dtype=t.dtype, device=t.device)
     if dist.get_backend(group) == "nccl":
+        out = torch.empty((world, *t.shape), dtype=t.dtype, device=t.device)
         dist.all_gather_into_tensor(out, t, group=group)
-    else:  # gloo (CPU tests)
-        dist.all_gather(list(out.unbind(0)), t, group=group)
-    return out
+        return out
+    # gloo (CPU tests; several ranks sharing one GPU in the 2-process session test): through the host
+    host = t.cpu()
+    out = torch.empty((world, *t.shape), dtype=t.dtype)
+    dist.all_gather(list(out.unbind(0)), host, group=group)
+    return out.to(t.device)
 
 
 def gather_head_outputs(local: torch.Tensor, group=None) -> torch.Tensor:
@@ -251,11 +254,21 @@ def rebalance_plan(old_owners, new_owners, rank: int):
 
 def exchange_frames(sends, recvs, group=None) -> None:
     """Point-to-point moves of frame rows: ``sends`` / ``recvs`` are lists of
-    (peer, tensor) in the same global order on both sides of every pair."""
+    (peer, tensor) in the same global order on both sides of every pair.
+    NCCL moves device rows directly (NVLink); gloo stages them through the host."""
+    if not sends and not recvs:
+        return
+    if dist.get_backend(group) != "nccl":
+        host_recv = [(peer, torch.empty(t.shape, dtype=t.dtype)) for peer, t in recvs]
+        ops = [dist.P2POp(dist.isend, t.contiguous().cpu(), peer, group) for peer, t in sends]
+        ops += [dist.P2POp(dist.irecv, h, peer, group) for peer, h in host_recv]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        for (_, dst), (_, h) in zip(recvs, host_recv):
+            dst.copy_(h)
+        return
     ops = [dist.P2POp(dist.isend, t, peer, group) for peer, t in sends]
     ops += [dist.P2POp(dist.irecv, t, peer, group) for peer, t in recvs]
-    if not ops:
-        return
     for req in dist.batch_isend_irecv(ops):
         req.wait()
 

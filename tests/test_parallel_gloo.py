@@ -163,3 +163,53 @@ def test_lpt_owners_balance():
     assert (P.lpt_owners(costs, 1) == 0).all()
     with pytest.raises(df.ConfigError):
         P.lpt_owners(costs[0], 2)
+
+
+def test_bench_gpus_n_starts_n_ranks():
+    """``bench.py --gpus 2`` without a launcher re-executes itself under torchrun, one rank per GPU
+    (the --rank-check hook reports each rank's RANK / WORLD_SIZE and exits before touching a GPU)."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--rank-check"],
+                         capture_output=True, text=True, timeout=300, check=True).stdout
+    lines = sorted((json.loads(l) for l in out.splitlines() if l.startswith("{")), key=lambda d: d["rank"])
+    assert lines == [{"rank": 0, "world": 2}, {"rank": 1, "world": 2}]
+    # a launcher whose world size disagrees with --gpus is refused
+    bad = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "4", "--rank-check"],
+                         capture_output=True, text=True, timeout=120, env=dict(os.environ, WORLD_SIZE="2"))
+    assert bad.returncode != 0 and "WORLD_SIZE=2" in bad.stderr
+
+
+def test_fused_gather_buffers_alternate_per_gather_with_odd_layer_count():
+    """The fused all-gather's two symmetric buffers alternate once per gather, not by layer index:
+    with an odd layer count, layer L-1 of one denoise iteration and layer 0 of the next write
+    different buffers, so a fast rank never stores into the buffer a slow rank still reads."""
+    calls = []
+
+    class _H:
+        def __init__(self, i):
+            self.i = i
+
+        def barrier(self, channel=0):
+            calls.append(self.i)
+
+    fg = object.__new__(P.FusedHeadGather)
+    fg.bufs = [torch.zeros(2, 2), torch.zeros(2, 2)]
+    fg.handles = [_H(0), _H(1)]
+    fg.peers = [[11], [22]]
+    fg.turn = 0
+    L, iters = 3, 3
+    used = []
+    for _ in range(iters):
+        for layer in range(L):
+            tgt = fg.target(layer, [0])
+            assert tgt.out is fg.current()
+            used.append(fg.bufs.index(tgt.out) if tgt.out is fg.bufs[0] else 1)
+            assert tgt.peers == fg.peers[used[-1]]
+            fg.barrier()
+    assert used == [i % 2 for i in range(L * iters)]
+    assert calls == used
+    assert all(a != b for a, b in zip(used, used[1:]))
