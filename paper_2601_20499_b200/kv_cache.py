@@ -332,27 +332,30 @@ class HeadKVCache:
         if not _same_staging(self._staged, block, slot, st.arena):
             segs = _block_segments(block, st, slot, dev)
         self._staged = None
-        self._slot_frame[slot] = block.frame_id
-        keep = set(self.policy.retain(self.frame_ids))
-        self._slot_frame = [f if (f is not None and f in keep) else None for f in self._slot_frame]
-        segs += self._compact()
-        return segs
-
-    def _compact(self) -> list[tuple]:
-        """Restore the prefix invariant (occupied + pending == [0, len+1))."""
-        segs = []
-        st = self.storage
-        while True:
-            n = len(self)
-            high = [s for s, f in enumerate(self._slot_frame) if f is not None and s > n]
-            if not high:
-                return segs
-            src = max(high)
-            dst = self.pending_slot
+        for src, dst in self._append_slots(block.frame_id):
             for plane in (st.arena.k, st.arena.v):
                 a, b = plane[st.rows(src)], plane[st.rows(dst)]
                 segs.append((a.data_ptr(), b.data_ptr(), st.hw, st.arena.width * 2, st.arena.width * 2,
                              st.arena.width * 2))
+        return segs
+
+    def _append_slots(self, frame_id: int) -> list[tuple[int, int]]:
+        """Slot-table half of an append: ``frame_id`` takes the pending slot, the policy evicts
+        (kv_cache.py:187-197), then the prefix invariant (occupied + pending == [0, len+1)) is
+        restored by moving the highest occupied slots down.  Returns the (src, dst) slot moves.
+        A pure function of the table, so another process can replay a ring's layout."""
+        self._slot_frame[self.pending_slot] = frame_id
+        keep = set(self.policy.retain(self.frame_ids))
+        self._slot_frame = [f if (f is not None and f in keep) else None for f in self._slot_frame]
+        moves = []
+        while True:
+            n = len(self)
+            high = [s for s, f in enumerate(self._slot_frame) if f is not None and s > n]
+            if not high:
+                return moves
+            src = max(high)
+            dst = self.pending_slot
+            moves.append((src, dst))
             self._slot_frame[dst], self._slot_frame[src] = self._slot_frame[src], None
 
     def rebuild(self, policy: CachePolicy) -> "HeadKVCache":
@@ -387,6 +390,22 @@ def _same_staging(staged, block: FrameBlock, slot: int, arena) -> bool:
     fid, s, a, k, v, kv, vv = staged
     return (fid == block.frame_id and s == slot and a is arena and k is block.keys and v is block.values
             and (kv, vv) == _versions(block))
+
+
+def replay_slot_table(policy: CachePolicy, history: list[int], appended: list[int]) -> list[int | None]:
+    """The slot table of a ring rebuilt under ``policy`` from the frame ids ``history`` (rebuild_caches
+    lays the retained frames in frame order) and then appended ``appended`` -- what that ring holds in
+    which slot, computed without storage (a head-parallel rank receiving the ring lays the rows out
+    identically, so key order and hence the attention's summation order match the sender's)."""
+    n = HeadKVCache(policy)
+    kept: list[int] = []
+    for f in history:
+        kept = policy.retain(kept + [f])
+    for s, f in enumerate(kept):
+        n._slot_frame[s] = f
+    for f in appended:
+        n._append_slots(f)
+    return list(n._slot_frame)
 
 
 def rebuild_caches(caches: list[HeadKVCache], policies: list[CachePolicy], arena: K.KVArena | None = None,

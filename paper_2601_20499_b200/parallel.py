@@ -144,7 +144,7 @@ class HeadParallelSession(Session):
         import numpy as np
 
         from . import kernels as K
-        from .kv_cache import HeadKVCache, RingStorage, derive_policy, extension_window
+        from .kv_cache import HeadKVCache, RingStorage, derive_policy, extension_window, replay_slot_table
 
         cfg = self.config
         L, H = cfg.num_layers, cfg.num_heads
@@ -155,18 +155,15 @@ class HeadParallelSession(Session):
         new = lpt_owners(np.array([[p.ring_slots for p in row] for row in pol]), self.world)
         keep, send, recv = rebalance_plan(old, new, self.rank)
 
-        def kept(p) -> list[int]:  # rebuild under p, then the classifying step's append (kv_cache.py:187-201)
-            frames: list[int] = []
-            for f in self._history:
-                frames = p.retain(frames + [f])
-            return p.retain(frames + [frame_id])
+        def layout(p) -> list[int | None]:  # rebuild under p, then the classifying step's append
+            return replay_slot_table(p, self._history, [frame_id])
 
         h0 = self.head_range.start
         sends = []
         for l, h, dst in send:
             c = self.caches[l][h - h0]
-            if c.frame_ids != kept(pol[l][h]):
-                raise ConfigError(f"layer {l} head {h}: ring frames {c.frame_ids} != {kept(pol[l][h])}")
+            if c._slot_frame != layout(pol[l][h]):
+                raise ConfigError(f"layer {l} head {h}: ring slots {c._slot_frame} != {layout(pol[l][h])}")
             for f in c.frame_ids:
                 rows = c.storage.rows(c.slot_of(f))
                 sends += [(dst, c.storage.arena.k[rows]), (dst, c.storage.arena.v[rows])]
@@ -179,9 +176,9 @@ class HeadParallelSession(Session):
                 p = pol[l][h]
                 st = RingStorage(arena, arena.allocate(p.ring_slots * cfg.HW), p.ring_slots, cfg.HW, cfg.head_dim)
                 n = HeadKVCache(p, storage=st)
-                for slot, f in enumerate(kept(p)):
-                    n._slot_frame[slot] = f
-                    rows = st.rows(slot)
+                n._slot_frame = layout(p)  # the sender's slots: same key order in the ring
+                for f in n.frame_ids:  # frame order, as the sender sends
+                    rows = st.rows(n.slot_of(f))
                     recvs += [(src, arena.k[rows]), (src, arena.v[rows])]
                 incoming[(l, h)] = n
         torch.cuda.synchronize(self.device)  # the rings' last append is on the session stream
