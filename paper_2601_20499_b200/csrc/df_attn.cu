@@ -107,7 +107,7 @@ struct __align__(64) AttnParams {
 // Dev-only timeline of CTA 0 (clock64 stamps): softmax warps 4 / 8 (lane 0)
 // and the MMA issuer, first kTraceIters kv tiles.  Read with df_trace_fetch.
 constexpr int kTraceIters = 128;
-__device__ unsigned long long g_trace[3][kTraceIters][10];
+__device__ unsigned long long g_trace[4][kTraceIters][10];
 __device__ unsigned long long g_cta_time[1024][4];  // globaltimer ns at CTA start / main-loop end / CTA end, SM id
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -639,33 +639,69 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
 }
 
 // =====================================================================
-// CTA-pair variant (cta_group::2, d = 128).  A cluster of two CTAs on one
-// TPC computes M = 256 per MMA: each CTA owns 128 rows of every 256-row query
-// tile, half of every K tile (64 keys) and half of every V tile (64 columns);
-// the leader's single thread issues tcgen05.mma.cta_group::2 for both.  Per SM
-// this halves the K/V bytes staged by TMA and read by the tensor core, which
-// otherwise keep the shared-memory port saturated during QK^T.  Work item =
-// (head, 512 query rows, kv piece); MMA tile t covers rows [t*256, t*256+256)
-// of the item, CTA rank r rows [t*256 + r*128, +128).
+// CTA-pair variant (cta_group::2, d = 128): three softmax warpgroups in a ring.
+//
+// A cluster of two CTAs on one TPC computes M = 256 query rows per MMA: CTA
+// rank r owns rows [r*128, r*128+128) of the item's 256-row query tile, half of
+// every K tile (64 keys) and half of every V tile (64 columns); the leader's MMA
+// warp issues tcgen05.mma.cta_group::2 for both.  Work item = (head, 256 query
+// rows, kv piece) -- the 1-CTA kernel's granularity, on half as many bins.
+//
+// Why: in the 1-CTA kernel a query tile's next QK^T waits for the PV that
+// consumes its P (P aliases S and TMEM holds only S0 S1 O0 O1), so each softmax
+// warpgroup idles ~1200 cycles per kv tile (clock64 trace).  With 128 rows per
+// CTA, TMEM holds THREE score buffers and one O:
+//   S_0 [0,128)  S_1 [128,256)  S_2 [256,384)  O [384,512)
+// Three softmax warpgroups take the kv tiles in turn (tile j -> WG j%3, buffer
+// j%3; P overwrites the first 64 columns of its S buffer).  The MMA warp issues
+//   QK_0 QK_1 QK_2, then per tile j:  PV_j | QK_{j+3}
+// so two score tiles are always computed ahead, and a warpgroup's next S (three
+// tiles on) lands while the other two groups work.  The running max m is one per
+// row: each WG hands the m after its tile to the next WG of the ring (named
+// barrier per TMEM lane quadrant), which rescales its own partial row sum when m
+// moved; the lazy O rescale (threshold 2^16) waits for the previous PV.  A WG
+// reads its S in two passes (row max, then exponentials 32 columns at a time), so
+// the 14-warp CTA fits in 144 registers per thread.
+//
+// Warps: 0 TMA producer, 1 TMEM allocator + MMA issuer (leader CTA), 2-13 the
+// softmax groups (WG g = warps 2+4g .. 5+4g; warp w reads TMEM lane quadrant w%4).
+constexpr int kPairWarps = 14;
+constexpr int kPairThreads = kPairWarps * 32;
+
 struct PairCfg {
   static constexpr int D = 128;
-  static constexpr int kStages = 4;                      // K and V ring depth
-  static constexpr int kQTileBytes = 128 * D * 2;        // this CTA's rows of one MMA tile
-  static constexpr int kQBoxBytes = 128 * 128;           // [128 rows x 64 cols]
-  static constexpr int kKHalfBytes = 64 * D * 2;         // 64 keys x d
-  static constexpr int kKBoxBytes = 64 * 128;            // [64 rows x 64 cols]
-  static constexpr int kVHalfBytes = 128 * 64 * 2;       // 128 keys x 64 columns
+#ifndef DF_PAIR_STAGES_K
+#define DF_PAIR_STAGES_K 5
+#endif
+#ifndef DF_PAIR_STAGES_V
+#define DF_PAIR_STAGES_V 4
+#endif
+  static constexpr int kStagesK = DF_PAIR_STAGES_K;  // K ring depth
+  static constexpr int kStagesV = DF_PAIR_STAGES_V;  // V ring depth
+  static constexpr int kKAhead = 3;                  // K loads lead V loads by this many tiles (QK_{j+3} before PV_j)
+  static constexpr int kQBytes = 128 * D * 2;        // this CTA's 128 query rows
+  static constexpr int kQBoxBytes = 128 * 128;       // [128 rows x 64 cols]
+  static constexpr int kKHalfBytes = 64 * D * 2;     // 64 keys x d
+  static constexpr int kKBoxBytes = 64 * 128;        // [64 rows x 64 cols]
+  static constexpr int kVHalfBytes = 128 * 64 * 2;   // 128 keys x 64 columns
   static constexpr int kQOff = 0;
-  static constexpr int kKOff = 2 * kQTileBytes;
-  static constexpr int kVOff = kKOff + kStages * kKHalfBytes;
-  static constexpr int kBarOff = kVOff + kStages * kVHalfBytes;
-  static constexpr int kNumBars = 1 + 4 * kStages + 2 + 4 + 2;
+  static constexpr int kKOff = kQBytes;
+  static constexpr int kVOff = kKOff + kStagesK * kKHalfBytes;
+  static constexpr int kXOff = kVOff + kStagesV * kVHalfBytes;  // m handoff [128], final m [128], [3 WG][4][128] sums
+  static constexpr int kXBytes = (128 + 128 + 3 * 4 * 128) * 4;
+  static constexpr int kBarOff = kXOff + kXBytes;
+  static constexpr int kNumBars = 1 + 2 * kStagesK + 2 * kStagesV + 3 + 6 + 3;
   static constexpr int kSmem = kBarOff + kNumBars * 8 + 32 + 1024;
-  static constexpr uint32_t kTmemO = 256;
+  static constexpr uint32_t kTO = 384;
 };
 
+// Named barriers of the pair kernel (64 threads: one warp of each of two WGs):
+// m handoff out of WG g for lane quadrant q: 2 + 4g + q.  Id 1 spans all softmax warps.
+__device__ __forceinline__ void nbar_arrive64(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void nbar_sync64(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+
 template <bool kProbe>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     df_attn_pair_kernel(const __grid_constant__ AttnParams p) {
   using C = PairCfg;
   constexpr int D = C::D;
@@ -674,14 +710,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
   uint64_t* q_full = bars;
   uint64_t* k_full = q_full + 1;
-  uint64_t* k_empty = k_full + C::kStages;
-  uint64_t* v_full = k_empty + C::kStages;
-  uint64_t* v_empty = v_full + C::kStages;
-  uint64_t* s_full = v_empty + C::kStages;  // [2]
-  uint64_t* p_full = s_full + 2;            // [2 tiles][2 halves], leader: 128 + 128 arrivals
-  uint64_t* o_full = p_full + 4;            // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+  uint64_t* k_empty = k_full + C::kStagesK;
+  uint64_t* v_full = k_empty + C::kStagesK;
+  uint64_t* v_empty = v_full + C::kStagesV;
+  uint64_t* s_full = v_empty + C::kStagesV;  // [3] S buffer written (multicast commit)
+  uint64_t* p_full = s_full + 3;             // [3 buffers][2 halves] leader: 8 warp arrivals
+  uint64_t* pv_done = p_full + 6;            // [3] PV from that buffer landed (multicast commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 3);
   int32_t* last_flag = reinterpret_cast<int32_t*>(tmem_slot + 1);
+  float* m_x = reinterpret_cast<float*>(smem + C::kXOff);  // [128] m handoff
+  float* m_fin = m_x + 128;                                 // [128] final m
+  float* l_x = m_fin + 128;                                 // [3 WG][4: l, 3 region masses][128]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -693,30 +732,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const HeadParam hd = p.heads[h];
   const int local = pair - p.item_prefix[hrank];
   const int ns = hd.n_split;
-  const int qp = local / ns;
-  const int piece = local - qp * ns;
+  const int qt = local / ns;
+  const int piece = local - qt * ns;
   const int n_kv_total = (hd.n_tok + kBN - 1) / kBN;
   const int kv_begin = (piece * n_kv_total) / ns;
   const int n_kv = ((piece + 1) * n_kv_total) / ns - kv_begin;
-  const bool two = qp * 4 * kBM + 2 * kBM < p.hw;  // second 256-row tile has rows
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < C::kStages; ++s) {
+    for (int s = 0; s < C::kStagesK; ++s) {
       mbar_init(k_full + s, 1);
       mbar_init(k_empty + s, 1);
+    }
+    for (int s = 0; s < C::kStagesV; ++s) {
       mbar_init(v_full + s, 1);
       mbar_init(v_empty + s, 1);
     }
-    for (int t = 0; t < 2; ++t) {
-      mbar_init(s_full + t, 1);
-      mbar_init(p_full + 2 * t, 8);  // one arrival per softmax warp of either CTA
-      mbar_init(p_full + 2 * t + 1, 8);
-      mbar_init(o_full + t, 1);
+    for (int b = 0; b < 3; ++b) {
+      mbar_init(s_full + b, 1);
+      mbar_init(p_full + 2 * b, 8);  // one arrival per softmax warp of either CTA
+      mbar_init(p_full + 2 * b + 1, 8);
+      mbar_init(pv_done + b, 1);
     }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   tc_fence_before();
   cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
   tc_fence_after();
@@ -731,174 +772,236 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       prefetch_tmap(kmap);
       prefetch_tmap(vmap);
       const uint64_t keep = policy_evict_last();
-      const int nq = two ? 2 : 1;
-      const int qrow0 = hd.q_head * p.hw + qp * 4 * kBM + static_cast<int>(crank) * kBM;
-      if (crank == 0) mbar_expect_tx(q_full, nq * 2 * C::kQTileBytes);
+      const int qrow0 = hd.q_head * p.hw + qt * 2 * kBM + static_cast<int>(crank) * kBM;
+      if (crank == 0) mbar_expect_tx(q_full, 2 * C::kQBytes);
       const uint32_t lq = mapa_shared(smem_u32(q_full), 0);
-      for (int t = 0; t < nq; ++t)
-        for (int b = 0; b < 2; ++b)
-          tma_load_2d_pair(smem + C::kQOff + t * C::kQTileBytes + b * C::kQBoxBytes, &p.qmap, lq, b * 64,
-                           qrow0 + t * 2 * kBM, keep);
-      for (int jj = 0; jj < n_kv; ++jj) {
-        const int row = hd.base_row + (kv_begin + jj) * kBN;
-        const int s = jj % C::kStages;
-        const uint32_t ph = (jj / C::kStages) & 1;
-        mbar_wait_cluster(k_empty + s, ph ^ 1);
+      for (int b = 0; b < 2; ++b)
+        tma_load_2d_pair(smem + C::kQOff + b * C::kQBoxBytes, &p.qmap, lq, b * 64, qrow0, keep);
+      // K runs kKAhead tiles ahead of V (QK_{j+3} is issued right after PV_j)
+      auto load_k = [&](int jj) {
+        const int s = jj % C::kStagesK;
+        mbar_wait(k_empty + s, ((jj / C::kStagesK) & 1) ^ 1);
         if (crank == 0) mbar_expect_tx(k_full + s, 2 * C::kKHalfBytes);
         const uint32_t lk = mapa_shared(smem_u32(k_full + s), 0);
+        const int row = hd.base_row + (kv_begin + jj) * kBN + static_cast<int>(crank) * 64;
         for (int b = 0; b < 2; ++b)
-          tma_load_2d_pair(smem + C::kKOff + s * C::kKHalfBytes + b * C::kKBoxBytes, kmap, lk, b * 64,
-                           row + static_cast<int>(crank) * 64, keep);
-        mbar_wait_cluster(v_empty + s, ph ^ 1);
+          tma_load_2d_pair(smem + C::kKOff + s * C::kKHalfBytes + b * C::kKBoxBytes, kmap, lk, b * 64, row, keep);
+      };
+      auto load_v = [&](int jj) {
+        const int s = jj % C::kStagesV;
+        mbar_wait(v_empty + s, ((jj / C::kStagesV) & 1) ^ 1);
         if (crank == 0) mbar_expect_tx(v_full + s, 2 * C::kVHalfBytes);
         const uint32_t lv = mapa_shared(smem_u32(v_full + s), 0);
-        tma_load_2d_pair(smem + C::kVOff + s * C::kVHalfBytes, vmap, lv, static_cast<int>(crank) * 64, row, keep);
+        tma_load_2d_pair(smem + C::kVOff + s * C::kVHalfBytes, vmap, lv, static_cast<int>(crank) * 64,
+                         hd.base_row + (kv_begin + jj) * kBN, keep);
+      };
+      for (int jj = 0; jj < n_kv + C::kKAhead; ++jj) {
+        if (jj < n_kv) load_k(jj);
+        if (jj >= C::kKAhead) load_v(jj - C::kKAhead);
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader CTA)
-    // Warp-wide loop, elected lane issues, precomputed descriptor bases (as df_attn_kernel).
     if (crank == 0) {
       constexpr uint32_t idesc_qk = idesc_bf16(2 * kBM, kBN, false);
       constexpr uint32_t idesc_pv = idesc_bf16(2 * kBM, D, true);
       const uint64_t dQ = sdesc_sw128(smem_u32(smem + C::kQOff), 16, 1024);
       const uint64_t dK = sdesc_sw128(smem_u32(smem + C::kKOff), 16, 1024);
       const uint64_t dV = sdesc_sw128(smem_u32(smem + C::kVOff), 16, 1024);
-      const uint32_t tS0 = tmem, tS1 = tmem + 128;
-      const uint32_t tO0 = tmem + C::kTmemO, tO1 = tmem + C::kTmemO + D;
+      const uint32_t tO = tmem + C::kTO;
 
-      auto qk = [&](uint32_t d_tmem, int t, int ks) {
-        const uint64_t qa = dQ + ((t * C::kQTileBytes) >> 4);
-        const uint64_t kb = dK + ((ks * C::kKHalfBytes) >> 4);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint64_t oa = ((kk >> 2) * C::kQBoxBytes + (kk & 3) * 32) >> 4;
-          const uint64_t ob = ((kk >> 2) * C::kKBoxBytes + (kk & 3) * 32) >> 4;
-          umma_ss_pair_elect(d_tmem, qa + oa, kb + ob, idesc_qk, kk > 0);
-        }
-      };
-      auto pv = [&](int t, int jj) {
-        const int vs = jj % C::kStages;
-        mbar_wait_cluster(p_full + 2 * t, jj & 1);
+      auto qk = [&](int j) {  // S_{j%3} = Q K_j^T; in pipe order after PV_{j-3}, which read P from that buffer
+        const int ks = j % C::kStagesK;
+        const int b = j % 3;
+        mbar_wait(k_full + ks, (j / C::kStagesK) & 1);
         tc_fence_after();
-        if (t == 0) {
-          mbar_wait_cluster(v_full + vs, (jj / C::kStages) & 1);
-          tc_fence_after();
-        }
-        const uint64_t vb = dV + ((vs * C::kVHalfBytes) >> 4);
-        const uint32_t tP = t ? tS1 : tS0;
-        const uint32_t tO = t ? tO1 : tO0;
-#pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk) {
-          if (kk == kBN / 32) {
-            mbar_wait_cluster(p_full + 2 * t + 1, jj & 1);
-            tc_fence_after();
-          }
-          umma_ts_pair_elect(tO, tP + kk * 8, vb + ((kk * 2048) >> 4), idesc_pv, (jj > 0 || kk > 0) ? 1u : 0u);
-        }
-        umma_commit_pair_elect(o_full + t);
-        if (t == 1 || !two) umma_commit_pair_elect(v_empty + vs);
-      };
-
-      mbar_wait_cluster(q_full, 0);
-      tc_fence_after();
-      for (int jj = 0; jj < n_kv; ++jj) {
-        const int ks = jj % C::kStages;
-        if (lane == 0) DF_STAMP(2, jj, 0);
-        mbar_wait_cluster(k_full + ks, (jj / C::kStages) & 1);
-        tc_fence_after();
-        if (lane == 0) DF_STAMP(2, jj, 1);
-        qk(tS0, 0, ks);
-        umma_commit_pair_elect(s_full + 0);
-        if (two) {
-          if (lane == 0) DF_STAMP(2, jj, 2);
-          if (jj > 0) pv(1, jj - 1);
-          if (lane == 0) DF_STAMP(2, jj, 3);
-          qk(tS1, 1, ks);
-          umma_commit_pair_elect(s_full + 1);
-        }
+        if (lane == 0) DF_STAMP(3, j, 0);
+        static_assert(C::kQBoxBytes >> 4 == 1024 && C::kKBoxBytes >> 4 == 512, "umma_ss_pair_qk8 offsets");
+#ifndef DF_DIAG_NO_MMA
+        umma_ss_pair_qk8(tmem + b * 128, dQ, dK + ((ks * C::kKHalfBytes) >> 4), idesc_qk);
+#endif
+        umma_commit_pair_elect(s_full + b);
         umma_commit_pair_elect(k_empty + ks);
-        if (lane == 0) DF_STAMP(2, jj, 4);
-        pv(0, jj);
-        if (lane == 0) DF_STAMP(2, jj, 5);
+      };
+      auto pv = [&](int j) {  // O += P_{j%3} V_j
+        const int vs = j % C::kStagesV;
+        const int b = j % 3;
+        const uint32_t ph = (j / 3) & 1;
+        mbar_wait(p_full + 2 * b, ph);  // keys 0-63 of P(j)
+        mbar_wait(v_full + vs, (j / C::kStagesV) & 1);
+        tc_fence_after();
+        if (lane == 0) DF_STAMP(3, j, 1);
+        const uint64_t vb = dV + ((vs * C::kVHalfBytes) >> 4);
+        const uint32_t tP = tmem + b * 128;
+#ifndef DF_DIAG_NO_MMA
+        umma_ts_pair_pv4(tO, tP, vb, idesc_pv, j > 0 ? 1u : 0u);
+#endif
+        mbar_wait(p_full + 2 * b + 1, ph);  // keys 64-127
+        tc_fence_after();
+#ifndef DF_DIAG_NO_MMA
+        umma_ts_pair_pv4(tO, tP + 32, vb + ((4 * 2048) >> 4), idesc_pv, 1u);
+#endif
+        umma_commit_pair_elect(pv_done + b);
+        umma_commit_pair_elect(v_empty + vs);
+        if (lane == 0) DF_STAMP(3, j, 2);
+      };
+
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      for (int j = 0; j < 3 && j < n_kv; ++j) qk(j);
+      for (int j = 0; j < n_kv; ++j) {
+        pv(j);
+        if (j + 3 < n_kv) qk(j + 3);
       }
-      if (two) pv(1, n_kv - 1);
     }
-  } else if (warp >= 4 && (two || warp < 8)) {
+  } else {
     // ------------------------------------------------------------ softmax (both CTAs)
-    const int t = (warp - 4) >> 2;
-    const int quad = warp & 3;
+    const int wg = (warp - 2) >> 2;  // tiles j with j % 3 == wg, score buffer wg
+    const int quad = warp & 3;       // TMEM lane quadrant of this warp
     const int row_local = quad * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-    const uint32_t tS = tmem + lane_off + t * 128;
-    const uint32_t tO = tmem + lane_off + C::kTmemO + t * D;
-    const uint32_t lp0 = mapa_shared(smem_u32(p_full + 2 * t), 0);
-    const uint32_t lp1 = mapa_shared(smem_u32(p_full + 2 * t + 1), 0);
-    auto arrive_p = [&](int half) {  // the leader's warps arrive locally, the peer's remotely
+    const uint32_t tS = tmem + lane_off + wg * 128;  // S, then P in its first 64 columns
+    const uint32_t tO = tmem + lane_off + C::kTO;
+    const int bar_in = 2 + 4 * ((wg + 2) % 3) + quad;  // m handed over by the previous WG of the ring
+    const int bar_out = 2 + 4 * wg + quad;             // m handed to the next WG
+    auto arrive_leader = [&](uint64_t* bar) {          // one arrival per warp on the leader's barrier
       if (crank == 0)
-        mbar_arrive(p_full + 2 * t + half);
+        mbar_arrive(bar);
       else
-        mbar_arrive_cluster(half ? lp1 : lp0);
+        mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0));
     };
     const float sl2 = p.scale_log2;
-    float m = -INFINITY;
-    float l = 0.f;
-    float reg_acc[3] = {0.f, 0.f, 0.f};
+    float m = -INFINITY;  // the running max this WG last used (log2 units)
+    float l = 0.f;        // this WG's partial row sum, relative to m
+    float reg_acc[3] = {0.f, 0.f, 0.f};  // probe: sink / neighbor / current mass, relative to m
 
     const bool stamp = lane == 0 && quad == 0;
-    for (int jj = 0; jj < n_kv; ++jj) {
+    for (int jj = wg; jj < n_kv; jj += 3) {
       const int j = kv_begin + jj;
-      if (stamp) DF_STAMP(t, jj, 0);
-      mbar_wait_cluster(s_full + t, jj & 1);
+      const int use = jj / 3;
+      if (stamp) DF_STAMP(wg, use, 0);
+      mbar_wait(s_full + wg, use & 1);
       tc_fence_after();
-      if (stamp) DF_STAMP(t, jj, 1);
-      uint32_t r[128];
-      tmem_ld32(tS + 0, r + 0);
-      tmem_ld32(tS + 32, r + 32);
-      tmem_ld32(tS + 64, r + 64);
-      tmem_ld32(tS + 96, r + 96);
-      tmem_wait_ld();
-      if (stamp) DF_STAMP(t, jj, 2);
-      const int valid = hd.n_tok - j * kBN;
-      if (valid < kBN) {
-#pragma unroll
-        for (int c = 0; c < 128; ++c)
-          if (c >= valid) r[c] = __float_as_uint(-INFINITY);
+      if (stamp) DF_STAMP(wg, use, 1);
+      const int valid = hd.n_tok - j * kBN;  // keys of this tile inside the head's context
+#ifdef DF_DIAG_NO_SOFTMAX  // dev: tensor-pipe-only timing (P = whatever TMEM holds)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        arrive_leader(p_full + 2 * wg);
+        arrive_leader(p_full + 2 * wg + 1);
       }
-      const float m_tile = row_max128(r) * sl2;
-      if (stamp) DF_STAMP(t, jj, 3);
-      if (jj == 0) {
-        m = m_tile;
-      } else {
-        const bool need = m_tile > m + kRescaleThreshold;
-        if (__any_sync(0xffffffffu, need)) {
-          const float alpha = need ? ex2(m - m_tile) : 1.f;
-          if (need) m = m_tile;
-          l *= alpha;
-          if constexpr (kProbe) {
-            reg_acc[0] *= alpha;
-            reg_acc[1] *= alpha;
-            reg_acc[2] *= alpha;
-          }
-          mbar_wait_cluster(o_full + t, (jj - 1) & 1);
-          tc_fence_after();
+      continue;
+#endif
+      if (valid < kBN) {  // the head's last tile: -inf into the score columns past its context (rare)
+        for (int c0 = (valid / 32) * 32; c0 < kBN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tS + c0, r);
+          tmem_wait_ld();
 #pragma unroll
-          for (int c = 0; c < D / 16; ++c) {
-            uint32_t o[16];
-            tmem_ld16(tO + c * 16, o);
-            tmem_wait_ld();
+          for (int c = 0; c < 32; ++c)
+            if (c0 + c >= valid) r[c] = __float_as_uint(-INFINITY);
+          tmem_st32(tS + c0, r);
+        }
+        tmem_wait_st();
+      }
+      // pass 1: the row max of the tile, 64 columns per TMEM load
+      float mx;
+      {
+        uint32_t r[64];
+        tmem_ld32(tS + 0, r);
+        tmem_ld32(tS + 32, r + 32);
+        tmem_wait_ld();
+        float a0 = fmax3(__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]));
+        float a1 = fmax3(__uint_as_float(r[3]), __uint_as_float(r[4]), __uint_as_float(r[5]));
 #pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st16(tO + c * 16, o);
+        for (int c = 6; c < 62; c += 4) {
+          a0 = fmax3(a0, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+          a1 = fmax3(a1, __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
+        }
+        mx = fmax3(a0, a1, fmaxf(__uint_as_float(r[62]), __uint_as_float(r[63])));
+#ifdef DF_DIAG_HALF_MAX  // dev: pass 1 reads half the columns (TMEM-bandwidth experiment; wrong m)
+        if (false) {
+#else
+        if (valid > 64) {
+#endif
+          tmem_ld32(tS + 64, r);
+          tmem_ld32(tS + 96, r + 32);
+          tmem_wait_ld();
+          a0 = fmax3(mx, __uint_as_float(r[0]), __uint_as_float(r[1]));
+          a1 = fmax3(__uint_as_float(r[2]), __uint_as_float(r[3]), __uint_as_float(r[4]));
+#pragma unroll
+          for (int c = 5; c < 61; c += 4) {
+            a0 = fmax3(a0, __uint_as_float(r[c]), __uint_as_float(r[c + 1]));
+            a1 = fmax3(a1, __uint_as_float(r[c + 2]), __uint_as_float(r[c + 3]));
           }
-          tmem_wait_st();
+          mx = fmax3(a0, a1, fmax3(__uint_as_float(r[61]), __uint_as_float(r[62]), __uint_as_float(r[63])));
         }
       }
+      const float m_tile = mx * sl2;
+      if (stamp) DF_STAMP(wg, use, 2);
+      // the running max after the previous tile (the previous WG's), then this tile's
+      float m_prev = m;
+      if (jj > 0) {
+        nbar_sync64(bar_in);
+        m_prev = m_x[row_local];
+        if (m_prev != m) {  // another WG raised m since this WG's last tile
+          const float a = ex2(m - m_prev);
+          l *= a;
+          if constexpr (kProbe) {
+            reg_acc[0] *= a;
+            reg_acc[1] *= a;
+            reg_acc[2] *= a;
+          }
+        }
+      }
+      bool rescale = false;
+      float alpha = 1.f;
+      if (jj == 0) {
+        m = m_tile;
+      } else if (m_tile > m_prev + kRescaleThreshold) {
+        alpha = ex2(m_prev - m_tile);
+        m = m_tile;
+        rescale = true;
+      } else {
+        m = m_prev;
+      }
+      if (jj + 1 < n_kv) {
+        m_x[row_local] = m;
+        nbar_arrive64(bar_out);
+      }
+      if (stamp) DF_STAMP(wg, use, 5);
+      if (rescale) {
+        l *= alpha;
+        if constexpr (kProbe) {
+          reg_acc[0] *= alpha;
+          reg_acc[1] *= alpha;
+          reg_acc[2] *= alpha;
+        }
+      }
+      if (__any_sync(0xffffffffu, rescale)) {  // O *= alpha once PV_{jj-1} has landed
+        const int pb = (jj - 1) % 3;
+        mbar_wait(pv_done + pb, ((jj - 1) / 3) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < D / 16; ++c) {
+          uint32_t o[16];
+          tmem_ld16(tO + c * 16, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st16(tO + c * 16, o);
+        }
+        tmem_wait_st();
+      }
+      if (stamp) DF_STAMP(wg, use, 3);
+      // pass 2: exponentials 32 columns at a time (the next chunk's TMEM load in flight); P quarter q
+      // overwrites S columns [16q, 16q+16), which the chunks already read
       const float2 scale2 = make_float2(sl2, sl2);
       const float2 negm2 = make_float2(-m, -m);
       float2 sum2 = make_float2(0.f, 0.f);
-      float2 lo2 = make_float2(0.f, 0.f);
       float span = 0.f;
+      float2 lo2 = make_float2(0.f, 0.f);
       int next_b = 0, kind = 0, slot = 0;
       const bool wide = p.hw >= kBN;
       if constexpr (kProbe) {
@@ -907,13 +1010,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         next_b = (c0 / p.hw + 1) * p.hw - c0;
         kind = p.region_tab[h * p.max_slots + slot];
       }
+      uint32_t rb[2][32];
+      tmem_ld32(tS, rb[0]);
+      tmem_wait_ld();
 #pragma unroll
       for (int quarter = 0; quarter < 4; ++quarter) {
+        uint32_t* r = rb[quarter & 1];
+        if (quarter < 3) tmem_ld32(tS + (quarter + 1) * 32, rb[(quarter + 1) & 1]);
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int c = quarter * 32 + 2 * i;
-          const float2 x = fma2(make_float2(__uint_as_float(r[c]), __uint_as_float(r[c + 1])), scale2, negm2);
+          const float2 x = fma2(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), scale2, negm2);
           float2 e;
           if (emulated_pair(c / 2)) {
             e = exp2_poly2(x, p.exp_unit);
@@ -942,16 +1050,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
           }
         }
+        if (quarter < 3) tmem_wait_ld();  // chunk quarter+1 is in registers
         tmem_st16(tS + quarter * 16, pk);
-        if (quarter == 1) {
-          if (stamp) DF_STAMP(t, jj, 6);
+        if (quarter == 1) {  // keys 0-63 of P: PV_jj may start
           tmem_wait_st();
-          if (stamp) DF_STAMP(t, jj, 7);
           tc_fence_before();
           __syncwarp();
-          if (stamp) DF_STAMP(t, jj, 8);
-          if (lane == 0) arrive_p(0);  // one arrival per warp: no named barrier on the P path
-          if (stamp) DF_STAMP(t, jj, 4);
+          if (lane == 0) arrive_leader(p_full + 2 * wg);
 #if DF_SCHED_FENCE
           sched_fence(p.n_heads < 0, last_flag);
 #endif
@@ -974,17 +1079,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) arrive_p(1);
-      if (stamp) DF_STAMP(t, jj, 5);
+      if (lane == 0) arrive_leader(p_full + 2 * wg + 1);
+      if (stamp) DF_STAMP(wg, use, 4);
     }
 
     // ------------------------------------------------------------ epilogue
-    mbar_wait_cluster(o_full + t, (n_kv - 1) & 1);
+    // every WG brings its row sum to the final running max (the last tile's WG has it), then sums
+    const int last_wg = (n_kv - 1) % 3;
+    if (wg == last_wg) m_fin[row_local] = m;
+    softmax_bar_sync(12 * 32);
+    {
+      const float mf = m_fin[row_local];
+      const float a = (l > 0.f) ? ex2(m - mf) : 0.f;  // m = -inf (no tile): l is 0 and stays 0
+      float* mine = l_x + wg * 4 * 128;
+      mine[row_local] = l * a;
+      if constexpr (kProbe) {
+        mine[128 + row_local] = reg_acc[0] * a;
+        mine[256 + row_local] = reg_acc[1] * a;
+        mine[384 + row_local] = reg_acc[2] * a;
+      }
+      m = mf;
+    }
+    softmax_bar_sync(12 * 32);
+    l = l_x[row_local] + l_x[512 + row_local] + l_x[1024 + row_local];
+    if constexpr (kProbe) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        reg_acc[k] = l_x[(k + 1) * 128 + row_local] + l_x[512 + (k + 1) * 128 + row_local] +
+                     l_x[1024 + (k + 1) * 128 + row_local];
+    }
+    const int lb = (n_kv - 1) % 3;
+    mbar_wait(pv_done + lb, ((n_kv - 1) / 3) & 1);  // the last PV (PVs land in order)
     tc_fence_after();
-    const int prow = t * kBM + row_local;                                       // row within this CTA's 256
-    const int row = qp * 4 * kBM + t * 2 * kBM + static_cast<int>(crank) * kBM + row_local;  // row within the head
+    const int row = qt * 2 * kBM + static_cast<int>(crank) * kBM + row_local;  // row within the head
     const bool row_ok = row < p.hw;
-    __nv_bfloat16* orow = p.out + (static_cast<int64_t>(hd.o_head) * p.hw + row) * p.out_ld;
+    const int64_t orow_off = (static_cast<int64_t>(hd.o_head) * p.hw + row) * p.out_ld;
+    __nv_bfloat16* orow = p.out + orow_off;
+    const int c_lo = wg * (D / 2);  // WG 0 / 1 store output columns [c_lo, c_lo + 64); WG 2 the probe rows
     auto store_row = [&](const float* o, int c0, float scale) {
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
@@ -996,19 +1127,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           wv.z = pack_bf16x2(o[v * 8 + 4] * scale, o[v * 8 + 5] * scale);
           wv.w = pack_bf16x2(o[v * 8 + 6] * scale, o[v * 8 + 7] * scale);
           *reinterpret_cast<uint4*>(orow + col) = wv;
+#ifndef DF_NO_PEERS
+          for (int pi = 0; pi < p.n_peers; ++pi)  // fused all-gather: NVLink stores into the peers' buffers
+            *reinterpret_cast<uint4*>(p.peer_out[pi] + orow_off + col) = wv;
+#endif
         }
       }
     };
     if (ns == 1) {
       const float inv_l = 1.f / l;
+      if (wg < 2) {
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t o[32];
-        tmem_ld32(tO + c * 32, o);
-        tmem_wait_ld();
-        if (row_ok) store_row(reinterpret_cast<const float*>(o), c * 32, inv_l);
-      }
-      if constexpr (kProbe) {
+        for (int c = 0; c < D / 64; ++c) {
+          uint32_t o[32];
+          tmem_ld32(tO + c_lo + c * 32, o);
+          tmem_wait_ld();
+          if (row_ok) store_row(reinterpret_cast<const float*>(o), c_lo + c * 32, inv_l);
+        }
+      } else if constexpr (kProbe) {
         if (row_ok && p.row_sampled[row]) {
           float* dst = p.probe_rows + (static_cast<int64_t>(h) * p.hw + row) * 3;
           dst[0] = reg_acc[0] * inv_l;
@@ -1017,42 +1153,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
     } else {
-      // split-KV, per CTA of the pair: slot (piece, rank), counter (group, rank)
-      const int group = (hd.group_base + qp) * 2 + static_cast<int>(crank);
-      const int64_t slot0 = static_cast<int64_t>(hd.part_base) + static_cast<int64_t>(qp) * ns;
+      // split-KV, per CTA of the pair: slot (piece, rank), counter (group, rank); rows of a slot 256 apart
+      const int group = (hd.group_base + qt) * 2 + static_cast<int>(crank);
+      const int64_t slot0 = static_cast<int64_t>(hd.part_base) + static_cast<int64_t>(qt) * ns;
       auto slot_of = [&](int i) { return (slot0 + i) * 2 + crank; };
-      float* my_o = p.ws_o + (slot_of(piece) * 2 * kBM + prow) * D;
+      if (wg < 2) {
+        float* my_o = p.ws_o + (slot_of(piece) * 2 * kBM + row_local) * D;
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
-        uint32_t o[32];
-        tmem_ld32(tO + c * 32, o);
-        tmem_wait_ld();
+        for (int c = 0; c < D / 64; ++c) {
+          uint32_t o[32];
+          tmem_ld32(tO + c_lo + c * 32, o);
+          tmem_wait_ld();
 #pragma unroll
-        for (int v = 0; v < 8; ++v)
-          __stcg(reinterpret_cast<float4*>(my_o + c * 32 + v * 4),
-                 make_float4(__uint_as_float(o[4 * v]), __uint_as_float(o[4 * v + 1]), __uint_as_float(o[4 * v + 2]),
-                             __uint_as_float(o[4 * v + 3])));
+          for (int v = 0; v < 8; ++v)
+            __stcg(reinterpret_cast<float4*>(my_o + c_lo + c * 32 + v * 4),
+                   make_float4(__uint_as_float(o[4 * v]), __uint_as_float(o[4 * v + 1]),
+                               __uint_as_float(o[4 * v + 2]), __uint_as_float(o[4 * v + 3])));
+        }
+      } else {
+        float* my_ml = p.ws_ml + (slot_of(piece) * 2 * kBM + row_local) * 8;
+        __stcg(reinterpret_cast<float4*>(my_ml), make_float4(m, l, reg_acc[0], reg_acc[1]));
+        __stcg(my_ml + 4, reg_acc[2]);
       }
-      float* my_ml = p.ws_ml + (slot_of(piece) * 2 * kBM + prow) * 8;
-      __stcg(reinterpret_cast<float4*>(my_ml), make_float4(m, l, reg_acc[0], reg_acc[1]));
-      __stcg(my_ml + 4, reg_acc[2]);
       __threadfence();
-      const int nthreads = two ? 256 : 128;
-      softmax_bar_sync(nthreads);
-      if (threadIdx.x == 128) {
+      softmax_bar_sync(12 * 32);
+      if (threadIdx.x == 64) {
         const int prev = atomicAdd(p.ws_cnt + group, 1);
         *last_flag = (prev == ns - 1);
         if (prev == ns - 1) p.ws_cnt[group] = 0;
         __threadfence();
       }
-      softmax_bar_sync(nthreads);
+      softmax_bar_sync(12 * 32);
       if (*last_flag && row_ok) {
         float M = -INFINITY;
-        for (int i = 0; i < ns; ++i) M = fmaxf(M, __ldcg(p.ws_ml + (slot_of(i) * 2 * kBM + prow) * 8));
+        for (int i = 0; i < ns; ++i) M = fmaxf(M, __ldcg(p.ws_ml + (slot_of(i) * 2 * kBM + row_local) * 8));
         float den = 0.f;
         float racc[3] = {0.f, 0.f, 0.f};
         for (int i = 0; i < ns; ++i) {
-          const float* ml = p.ws_ml + (slot_of(i) * 2 * kBM + prow) * 8;
+          const float* ml = p.ws_ml + (slot_of(i) * 2 * kBM + row_local) * 8;
           const float ei = ex2(__ldcg(ml) - M);
           den += ei * __ldcg(ml + 1);
           if constexpr (kProbe) {
@@ -1062,26 +1200,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
         }
         const float inv = 1.f / den;
+        if (wg < 2) {
 #pragma unroll 1
-        for (int c = 0; c < D / 32; ++c) {
-          float acc[32];
+          for (int c = 0; c < D / 64; ++c) {
+            float acc[32];
 #pragma unroll
-          for (int q = 0; q < 32; ++q) acc[q] = 0.f;
-          for (int i = 0; i < ns; ++i) {
-            const float ei = ex2(__ldcg(p.ws_ml + (slot_of(i) * 2 * kBM + prow) * 8) - M);
-            const float* src = p.ws_o + (slot_of(i) * 2 * kBM + prow) * D + c * 32;
+            for (int q = 0; q < 32; ++q) acc[q] = 0.f;
+            for (int i = 0; i < ns; ++i) {
+              const float ei = ex2(__ldcg(p.ws_ml + (slot_of(i) * 2 * kBM + row_local) * 8) - M);
+              const float* src = p.ws_o + (slot_of(i) * 2 * kBM + row_local) * D + c_lo + c * 32;
 #pragma unroll
-            for (int v = 0; v < 8; ++v) {
-              const float4 x = __ldcg(reinterpret_cast<const float4*>(src + v * 4));
-              acc[4 * v + 0] += ei * x.x;
-              acc[4 * v + 1] += ei * x.y;
-              acc[4 * v + 2] += ei * x.z;
-              acc[4 * v + 3] += ei * x.w;
+              for (int v = 0; v < 8; ++v) {
+                const float4 x = __ldcg(reinterpret_cast<const float4*>(src + v * 4));
+                acc[4 * v + 0] += ei * x.x;
+                acc[4 * v + 1] += ei * x.y;
+                acc[4 * v + 2] += ei * x.z;
+                acc[4 * v + 3] += ei * x.w;
+              }
             }
+            store_row(acc, c_lo + c * 32, inv);
           }
-          store_row(acc, c * 32, inv);
-        }
-        if constexpr (kProbe) {
+        } else if constexpr (kProbe) {
           if (p.row_sampled[row]) {
             float* dst = p.probe_rows + (static_cast<int64_t>(h) * p.hw + row) * 3;
             dst[0] = racc[0] * inv;
@@ -1111,7 +1250,7 @@ static int launch_attn_pair(const AttnParams& p, int grid, cudaStream_t stream) 
     if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(df_attn_pair_kernel)", e);
     configured = true;
   }
-  kern<<<grid, kThreads, PairCfg::kSmem, stream>>>(p);
+  kern<<<grid, kPairThreads, PairCfg::kSmem, stream>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("df_attn_pair_kernel launch", e);
   return DF_OK;
@@ -1179,8 +1318,8 @@ struct Plan {
 };
 
 
-// rows of one work item: a pair of 128-row tiles, or 2 x 256 rows for the CTA-pair kernel
-inline int item_rows(bool pair) { return pair ? 512 : 256; }
+// rows of one work item: a pair of 128-row tiles (1-CTA kernel) or one 256-row MMA tile over a CTA pair
+inline int item_rows(bool) { return 256; }
 
 double simulate(const df_attn_args* a, const uint8_t* ns, const int* order, int sms, bool pair) {
   const int R = item_rows(pair);
@@ -1193,7 +1332,7 @@ double simulate(const df_attn_args* a, const uint8_t* ns, const int* order, int 
     const int h = order[r];
     const int tiles = (a->heads[h].n_tok + 127) / 128;
     for (int qp = 0; qp < nq; ++qp) {
-      const double f = (qp == nq - 1 && last_single) ? kSingleTileFactor : 1.0;
+      const double f = (qp == nq - 1 && last_single && !pair) ? kSingleTileFactor : 1.0;
       for (int s = 0; s < ns[h]; ++s) {
         const int len = ((s + 1) * tiles) / ns[h] - (s * tiles) / ns[h];
         double c = len * f + kPieceOverhead + (ns[h] > 1 ? kSplitOverhead : 0.0);
@@ -1424,8 +1563,6 @@ int validate(const df_attn_args* a) {
   for (int i = 0; i < a->n_peers; ++i)
     if (!a->peer_out[i] || (reinterpret_cast<uintptr_t>(a->peer_out[i]) & 15))
       return set_error(DF_E_ARG, "df_attn_fwd: peer_out[%d] null or not 16-byte aligned", i);
-  if (a->n_peers > 0 && (a->flags & DF_ATTN_PAIR))
-    return set_error(DF_E_ARG, "df_attn_fwd: peer outputs are not supported by the CTA-pair kernel");
   if (a->q_rows < 1 || a->q_rows > INT32_MAX) return set_error(DF_E_SHAPE, "df_attn_fwd: bad q_rows");
   if ((reinterpret_cast<uintptr_t>(a->q) & 15) || (reinterpret_cast<uintptr_t>(a->out) & 15) || (a->out_ld % 8))
     return set_error(DF_E_ARG, "df_attn_fwd: q/out must be 16-byte aligned, out_ld a multiple of 8");

@@ -411,3 +411,52 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 }
 
 }  // namespace dfb
+
+namespace dfb {
+// Blocks of pair MMAs issued by one elected lane in one asm statement: the
+// descriptor bases are converted to uniform registers once per block instead of
+// once per UMMA (the per-UMMA elect + R2UR sequence of the single-MMA wrappers
+// costs ~10 issue slots on a sub-partition shared with three softmax warps).
+// QK^T block of the CTA-pair kernel: 8 x (M=256, N=128, K=16); A = Q [2 boxes of 128 rows x 64 cols],
+// B = K half [2 boxes of 64 rows x 64 cols], both K-major SWIZZLE_128B (desc units of 16 B).
+__device__ __forceinline__ void umma_ss_pair_qk8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b64 a, b;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, 0;\n\t"
+      "add.s64 a, %1, 2;\n\tadd.s64 b, %2, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, 4;\n\tadd.s64 b, %2, 4;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, 6;\n\tadd.s64 b, %2, 6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, 1024;\n\tadd.s64 b, %2, 512;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, 1026;\n\tadd.s64 b, %2, 514;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, 1028;\n\tadd.s64 b, %2, 516;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t"
+      "add.s64 a, %1, 1030;\n\tadd.s64 b, %2, 518;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, 1;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc)
+      : "memory");
+}
+// Half of a PV block: 4 x (M=256, N=128, K=16) with A = P from TMEM (8 columns per 16 keys) and
+// B = V half (MN-major, 128 keys x 64 columns, 2048 B per 16 keys).
+__device__ __forceinline__ void umma_ts_pair_pv4(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                                 uint32_t accumulate_first) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b64 b;\n\t.reg .b32 a;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "add.u32 a, %1, 8;\n\tadd.s64 b, %2, 128;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, 1;\n\t"
+      "add.u32 a, %1, 16;\n\tadd.s64 b, %2, 256;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, 1;\n\t"
+      "add.u32 a, %1, 24;\n\tadd.s64 b, %2, 384;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, 1;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate_first)
+      : "memory");
+}
+}  // namespace dfb

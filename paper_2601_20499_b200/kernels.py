@@ -19,8 +19,8 @@ from . import _lib
 from .errors import ShapeError
 
 TOKEN_ALIGN = 128  # head regions start on a kv-tile boundary
-# d = 128 launches use the CTA-pair kernel (cta_group::2) unless disabled here or per call.
-USE_CTA_PAIR = os.environ.get("DF_CTA_PAIR", "0") == "1"
+# d = 128 launches use the CTA-pair kernel (cta_group::2) unless DF_CTA_PAIR=0 or per call (pair=False).
+USE_CTA_PAIR = os.environ.get("DF_CTA_PAIR", "1") == "1"
 SUPPORTED_WIDTHS = (64, 128)
 
 
