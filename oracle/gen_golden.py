@@ -203,6 +203,51 @@ def gen_planted_sessions():
     json.dump(out, open(os.path.join(OUT, "planted_sessions.json"), "w"))
 
 
+def gen_extension_sessions():
+    """Planted sessions with the enlarged-context policies (BASELINE configs[4]; kv_cache.py:104-158,
+    engine.py:390-405): context_extension (hma, packed), merged_window (hma) and both (hma).  Per AR
+    step the final denoise iteration's context frame list of every (layer, head) is recorded through
+    the reference's observer (engine.py:73-84), with the extension window, MACs, ratio, F, classes."""
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from conftest import planted_setup  # reference fixture helper (read-only import)
+
+    variants = [("hma", {"context_extension": True}), ("packed", {"context_extension": True}),
+                ("hma", {"merged_window": 5}), ("hma", {"merged_window": 3, "context_extension": True})]
+    out = []
+    for seed in range(3):
+        for ratio in (1.0, 0.25):
+            for mode, extra in variants:
+                cfg, spec = planted_setup(seed, margin=2.0, subsample_ratio=ratio)
+                cfg = ref.SessionConfig(**{**cfg.to_dict(), "ar_steps": 12, **extra})
+                frames_seen = {}
+
+                def observer(tr, frames_seen=frames_seen, cfg=cfg):
+                    if tr.denoise_step == cfg.denoise_steps - 1:
+                        frames_seen.setdefault(tr.ar_step, {})[tr.layer] = [list(c[3]) for c in tr.contexts]
+
+                s = ref.Session(planted_stream(spec, cfg), cfg, mode, observer=observer)
+                frames, rep = s.run()
+                table = ref_prof.global_scores(
+                    ref.Session(planted_stream(spec, cfg), cfg, "baseline"), subsample_ratio=ratio)
+                ext = ref_kv.extension_window(s.assignment, cfg) if cfg.context_extension else None
+                out.append({
+                    "seed": seed, "ratio": ratio, "mode": mode, "labels": list(spec.labels),
+                    "noise_seed": spec.noise_seed, "config": cfg.to_dict(),
+                    "F": table.scores.tolist(),
+                    "classes": [CODE[c] for c in s.assignment.classes],
+                    "objective": s.objective,
+                    "extension_window": ext,
+                    "cache_reduction_ratio": rep.cache_reduction_ratio,
+                    "kernel_calls_steady": rep.kernel_calls_steady,
+                    "step_macs": [st["key_token_macs"] for st in rep.steps],
+                    "context_frames": [[frames_seen[a][l] for l in range(cfg.num_layers)]
+                                       for a in range(cfg.ar_steps)],
+                    "frame_ids": [[c.frame_ids for c in layer] for layer in s.caches],
+                    "output_digest": rep.to_dict()["output_digest"],
+                })
+    json.dump(out, open(os.path.join(OUT, "extension_sessions.json"), "w"))
+
+
 def gen_accounting():
     out = {"macs": [], "subsample": [], "extension": [], "ratio": []}
     for (L, H, d, HW, W, sink), hist in [((2, 4, 64, 192, 6, 0), h) for h in range(0, 9)] + \
@@ -264,6 +309,7 @@ if __name__ == "__main__":
     gen_eviction()
     gen_attention()
     gen_planted_sessions()
+    gen_extension_sessions()
     gen_accounting()
     gen_toy_report()
     gen_container()

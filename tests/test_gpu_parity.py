@@ -98,6 +98,94 @@ def test_planted_sessions_match_reference():
         assert s.objective == pytest.approx(rec["objective"], abs=1e-3)
 
 
+def test_extension_sessions_match_reference():
+    """Enlarged context at fixed compute (BASELINE configs[4]): planted sessions with
+    context_extension (hma, packed), merged_window (hma) and both, through the device Session.
+    Classes / extension window / MACs / cache ratio / calls / frame ids bit-exact with the
+    reference (kv_cache.py:104-158, engine.py:390-405, tests/test_kv_cache.py:238-257), every
+    step's context frame list exact (the device rings rebuilt into 10-slot extended neighbor
+    rings), F within 1e-3, and every final-iteration layer output within 2e-2 of fp64 attention
+    on the device's own bf16 operands."""
+    for rec in json.load(open(os.path.join(G, "extension_sessions.json"))):
+        cfg = df.SessionConfig(**rec["config"])
+        stream = O.PlantedStream(rec["labels"], 2.0, rec["noise_seed"], O.Config(**rec["config"]))
+        seen = [[None] * cfg.num_layers for _ in range(cfg.ar_steps)]
+        worst = [0.0]
+
+        def observer(tr):
+            if tr.denoise_step != cfg.denoise_steps - 1:
+                return
+            seen[tr.ar_step][tr.layer] = [list(c[3]) for c in tr.contexts]
+            for h, (keys, values, _, _) in enumerate(tr.contexts):
+                ref = O.batched_attention(tr.q[h].double().cpu().numpy()[None], keys.double().cpu().numpy()[None],
+                                          values.double().cpu().numpy()[None], 1 / math.sqrt(cfg.head_dim))[0]
+                got = tr.outputs[h].float().cpu().numpy()
+                worst[0] = max(worst[0], float(np.abs(got - ref).max() / np.abs(ref).max()))
+
+        s = df.Session(stream, cfg, rec["mode"], observer=observer)
+        frames, rep = s.run()
+        tag = (rec["seed"], rec["ratio"], rec["mode"], cfg.context_extension, cfg.merged_window)
+        assert [df.head_programming.CODE_OF[c] for c in s.assignment.classes] == rec["classes"], tag
+        ext = df.extension_window(s.assignment, cfg) if cfg.context_extension else None
+        assert ext == rec["extension_window"], tag
+        F = s._probe_tables[(cfg.probe_ar_step, cfg.denoise_steps - 1, cfg.subsample_ratio)]
+        assert np.abs(F - np.array(rec["F"])).max() <= 1e-3, tag
+        assert rep.cache_reduction_ratio == rec["cache_reduction_ratio"], tag
+        assert rep.kernel_calls_steady == rec["kernel_calls_steady"], tag
+        assert [st["key_token_macs"] for st in rep.steps] == rec["step_macs"], tag
+        assert [[c.frame_ids for c in layer] for layer in s.caches] == rec["frame_ids"], tag
+        assert seen == rec["context_frames"], tag
+        assert worst[0] <= TOL, (tag, worst[0])
+        if ext is not None and rec["mode"] == "packed":  # neighbor rings hold the extended window
+            assert max(c.storage.slots for layer in s.caches for c in layer) == ext + 1
+
+
+def test_wan_shape_dhp_session_matches_oracle():
+    """C3 dynamic head programming at the Wan shape (HW 4680, d 128, W 6, ratio 0.25): a planted
+    2-layer x 12-head stream through the device Session, probe at AR step 2 with the fused DHP
+    epilogue.  F of every head within 1e-3 of the oracle's profiler restatement (profiler.py:147-170)
+    on the device's own bf16 probe operands; classes bit-exact with the oracle's greedy on that F and
+    equal to the planted labels; the classification-time pack and the next append move exact bytes
+    (every retained frame's K/V rows in the packed rings equal the rows the probe step attended to)."""
+    HW, d = 4680, 128
+    ocfg = O.Config(num_layers=2, num_heads=12, head_dim=d, HW=HW, window_len=6, ar_steps=4, denoise_steps=1,
+                    dummy_count=8, probe_ar_step=2, subsample_ratio=0.25)
+    labels = ("sink", "neighbor", "current", "neighbor", "current", "sink") * 4
+    stream = O.PlantedStream(labels, 2.0, O.derive(31, "planted"), ocfg)
+    cfg = df.SessionConfig(**ocfg.__dict__)
+    probe_ctx, later_ctx = {}, {}
+
+    def observer(tr):
+        if tr.ar_step == 2:
+            for h, (keys, values, lay, frames) in enumerate(tr.contexts):
+                probe_ctx[(tr.layer, h)] = (tr.q[h].cpu(), keys.cpu(), values.cpu(), list(frames))
+        elif tr.ar_step == 3:
+            for h, (keys, values, lay, frames) in enumerate(tr.contexts):
+                later_ctx[(tr.layer, h)] = (keys.cpu(), values.cpu(), list(frames))
+
+    s = df.Session(stream, cfg, "packed", observer=observer)
+    s.run()
+    F_dev = s._probe_tables[(2, 0, 0.25)]
+    F_ref = np.zeros_like(F_dev)
+    for (layer, h), (q, keys, _, frames) in probe_ctx.items():
+        kinds = ["sink" if f == 0 else "neighbor" for f in frames[:-1]] + ["current"]
+        F_ref[layer * 12 + h] = O.probe_scores(q.double().numpy(), keys.double().numpy(), kinds, HW, 0.25, d)
+    assert np.abs(F_dev - F_ref).max() <= 1e-3
+    codes, _ = O.greedy_classify(F_ref, cfg.dummy_count)
+    got = [df.head_programming.CODE_OF[c] for c in s.assignment.classes]
+    assert got == list(codes)
+    want = {"sink": df.HeadClass.SINK, "neighbor": df.HeadClass.NEIGHBOR, "current": df.HeadClass.DUMMY}
+    assert list(s.assignment.classes) == [want[x] for x in labels]
+    # packed + appended rings: each retained frame's rows at step 3 are the bytes the probe step saw
+    for (layer, h), (keys3, values3, frames3) in later_ctx.items():
+        _, keys2, values2, frames2 = probe_ctx[(layer, h)]
+        for i, f in enumerate(frames3[:-1]):
+            j = frames2.index(f)
+            assert torch.equal(keys3[i * HW:(i + 1) * HW], keys2[j * HW:(j + 1) * HW]), (layer, h, f)
+            assert torch.equal(values3[i * HW:(i + 1) * HW], values2[j * HW:(j + 1) * HW]), (layer, h, f)
+    assert s.pack_stats["bytes"] > 0
+
+
 def test_session_layer_outputs_match_oracle_on_device_operands():
     """Observer pattern: each layer's device output vs fp64 attention on the
     device's own bf16 context, C1-like shape (HW 192, d 64, W 6, 10 steps, 2 denoise)."""
