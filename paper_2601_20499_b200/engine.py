@@ -11,8 +11,10 @@ reported separately.
 
 from __future__ import annotations
 
+import contextlib
 import hashlib
 import math
+import os
 from dataclasses import dataclass, field
 from typing import Callable, Sequence
 
@@ -40,6 +42,21 @@ from .layout import FrameLayout
 from .profiler import Probe, subsample_rows
 
 MODES = ("baseline", "hma", "packed")
+# NVTX ranges per (AR step, denoise iteration, layer) and around classify / pack / append (SURVEY.md 5,
+# tracing) for nsys / ncu --nvtx; off unless DF_NVTX=1 (a range push/pop pair costs ~2 us of host time)
+NVTX = os.environ.get("DF_NVTX", "0") == "1"
+
+
+@contextlib.contextmanager
+def _nvtx(name: str):
+    if not NVTX:
+        yield
+        return
+    torch.cuda.nvtx.range_push(name)
+    try:
+        yield
+    finally:
+        torch.cuda.nvtx.range_pop()
 _HMA_GROUP_ORDER = (HeadClass.DUMMY, HeadClass.SINK, HeadClass.NEIGHBOR)
 
 
@@ -765,6 +782,10 @@ class Session:
         return m if x is None else x + m
 
     def _run_step(self, ar_step: int) -> None:
+        with _nvtx(f"ar{ar_step}"):
+            self._run_step_ranged(ar_step)
+
+    def _run_step_ranged(self, ar_step: int) -> None:
         cfg = self.config
         final_kv = []
         step_counters: list[StepCounters] = []
@@ -775,7 +796,8 @@ class Session:
             final = t == cfg.denoise_steps - 1
             ratios = sorted(self._probe_requests.get((ar_step, t), ()))
             if self._graphable(ratios):
-                x, blocks_all, counters = self._graph_iteration(x, ar_step, t)
+                with _nvtx(f"ar{ar_step}/denoise{t}/graph"):
+                    x, blocks_all, counters = self._graph_iteration(x, ar_step, t)
                 graphed = True
                 if final:  # the views are the pending ring slots; the frame id is this step's
                     final_kv = [[FrameBlock(ar_step, b.keys, b.values) for b in row] for row in blocks_all]
@@ -785,27 +807,29 @@ class Session:
             probes: dict[float, list[ProbeRequest]] = {r: [] for r in ratios}
             counters = StepCounters()
             for layer in range(cfg.num_layers):
-                q, blocks = self._project(layer, x, ar_step, t)
-                pr = None
-                if ratios:
-                    pr = self._probe_buffers(ratios[0])
-                    probes[ratios[0]].append(pr)
-                outputs, lc = self._layer_attention(layer, q, self.caches[layer], blocks, pr)
-                for extra in ratios[1:]:  # another ratio at the same key: re-run the probe epilogue
-                    pe = self._probe_buffers(extra)
-                    probes[extra].append(pe)
-                    self._layer_attention(layer, q, self.caches[layer], blocks, pe)
-                counters.add_layer(lc)
-                if self.observer is not None:
-                    self._notify(ar_step, t, layer, q, outputs, blocks)
-                if final:
-                    final_kv.append(blocks)
-                x = self._mix(layer, outputs, x)
+                with _nvtx(f"ar{ar_step}/denoise{t}/layer{layer}"):
+                    q, blocks = self._project(layer, x, ar_step, t)
+                    pr = None
+                    if ratios:
+                        pr = self._probe_buffers(ratios[0])
+                        probes[ratios[0]].append(pr)
+                    outputs, lc = self._layer_attention(layer, q, self.caches[layer], blocks, pr)
+                    for extra in ratios[1:]:  # another ratio at the same key: re-run the probe epilogue
+                        pe = self._probe_buffers(extra)
+                        probes[extra].append(pe)
+                        self._layer_attention(layer, q, self.caches[layer], blocks, pe)
+                    counters.add_layer(lc)
+                    if self.observer is not None:
+                        self._notify(ar_step, t, layer, q, outputs, blocks)
+                    if final:
+                        final_kv.append(blocks)
+                    x = self._mix(layer, outputs, x)
             for r in ratios:
                 self._finalize_probe((ar_step, t), r, probes[r])
             step_counters.append(counters)
         if self._classify_at is not None and self.assignment is None and ar_step == self._classify_at[0]:
-            self._classify()
+            with _nvtx(f"ar{ar_step}/classify+pack"):
+                self._classify()
         s = self.stream if self.stream is not None else torch.cuda.current_stream(self.device)
         segs = []
         for layer in range(cfg.num_layers):
@@ -814,7 +838,8 @@ class Session:
                 if self.shadow_caches is not None:
                     segs += self.shadow_caches[layer][h].append_segments(block, self.device)
         if segs:
-            launch_segments(segs, s)
+            with _nvtx(f"ar{ar_step}/append"):
+                launch_segments(segs, s)
         self._after_step(ar_step)
         frame = getattr(x, "f32", x)
         self._frames.append(frame.clone() if graphed else frame)  # graph buffers are reused by the next replay

@@ -237,3 +237,30 @@ def test_pair_and_single_cta_gemms_bitwise_equal(tmp_path, bn):
         b = torch.load(tmp_path / f"p1_{hw}.pt")
         for key in a:
             assert torch.equal(a[key], b[key]), (hw, key)
+
+
+def test_session_nvtx_ranges(monkeypatch):
+    """DF_NVTX tracing: one range per AR step, per (denoise iteration, layer), around the
+    classify + pack (and the append copies, which a projected model does not need), balanced push / pop."""
+    from paper_2601_20499_b200 import engine
+
+    pushed, depth = [], [0]
+
+    def push(name):
+        pushed.append(name)
+        depth[0] += 1
+
+    def pop():
+        depth[0] -= 1
+
+    monkeypatch.setattr(engine, "NVTX", True)
+    monkeypatch.setattr(torch.cuda.nvtx, "range_push", push)
+    monkeypatch.setattr(torch.cuda.nvtx, "range_pop", pop)
+    ocfg, toy = _toy_c1()
+    cfg = df.SessionConfig(**{**ocfg.__dict__, "ar_steps": 4})
+    df.Session(df.ProjectedModel(toy.weights, toy.frame_input, 4, 64, 192), cfg, "packed").run()
+    assert depth[0] == 0
+    assert [n for n in pushed if "/" not in n] == [f"ar{i}" for i in range(4)]
+    assert "ar0/denoise1/layer1" in pushed and "ar2/classify+pack" in pushed
+    assert not any(n.endswith("/append") for n in pushed)  # the projections wrote K/V into the rings: no copy
+    assert sum(n.endswith("/layer0") for n in pushed) == cfg.ar_steps * cfg.denoise_steps
