@@ -7,7 +7,9 @@
 // and, with DF_ATTN_PROBE, the probe recompute + region reduction of
 //   profiler.py:105-129 (frame_attention_scores), profiler.py:147-170.
 //
-// Work item = (head, pair of 128-row query tiles).  Each head attends to its
+// Two kernels: df_attn_pair_kernel (CTA pair, d = 128, the default; see its
+// header below) and df_attn_kernel (one CTA, d = 64 and DF_ATTN_SINGLE_CTA),
+// described here.  Work item = (head, pair of 128-row query tiles).  Each head attends to its
 // own contiguous token range of a KV arena (cached frames + current frame), so
 // a dummy head with a 2-frame context issues 2/7 of the K/V tiles of a
 // baseline head: no masked tiles are ever loaded or multiplied.
