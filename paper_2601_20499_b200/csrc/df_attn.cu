@@ -667,7 +667,8 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
 //
 // Warps: 0 TMA producer, 1 TMEM allocator + MMA issuer (leader CTA), 2-13 the
 // softmax groups (WG g = warps 2+4g .. 5+4g; warp w reads TMEM lane quadrant w%4).
-constexpr int pair_threads(int wgs) { return (2 + 4 * wgs) * 32; }
+constexpr int kPairWarps = 14;
+constexpr int kPairThreads = kPairWarps * 32;
 
 struct PairCfg {
   static constexpr int D = 128;
@@ -701,10 +702,8 @@ struct PairCfg {
 __device__ __forceinline__ void nbar_arrive64(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
 __device__ __forceinline__ void nbar_sync64(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
-// kWG softmax warpgroups: 3 (two-pass softmax, 128 registers per thread) or 2 (one TMEM read of S per
-// tile into 128 registers, ~200 registers per thread); both over the same three score buffers.
-template <bool kProbe, int kWG>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kWG), 1)
+template <bool kProbe>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     df_attn_pair_kernel(const __grid_constant__ AttnParams p) {
   using C = PairCfg;
   constexpr int D = C::D;
@@ -859,13 +858,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kWG), 1
     }
   } else {
     // ------------------------------------------------------------ softmax (both CTAs)
-    const int wg = (warp - 2) >> 2;  // tiles j with j % kWG == wg; tile j uses score buffer j % 3
+    const int wg = (warp - 2) >> 2;  // tiles j with j % 3 == wg, score buffer wg
     const int quad = warp & 3;       // TMEM lane quadrant of this warp
     const int row_local = quad * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t tS = tmem + lane_off + wg * 128;  // S, then P in its first 64 columns
     const uint32_t tO = tmem + lane_off + C::kTO;
-    const int bar_in = 2 + 4 * ((wg + kWG - 1) % kWG) + quad;  // m handed over by the previous WG of the ring
-    const int bar_out = 2 + 4 * wg + quad;                     // m handed to the next WG
+    const int bar_in = 2 + 4 * ((wg + 2) % 3) + quad;  // m handed over by the previous WG of the ring
+    const int bar_out = 2 + 4 * wg + quad;             // m handed to the next WG
     auto arrive_leader = [&](uint64_t* bar) {          // one arrival per warp on the leader's barrier
       if (crank == 0)
         mbar_arrive(bar);
@@ -878,13 +878,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kWG), 1
     float reg_acc[3] = {0.f, 0.f, 0.f};  // probe: sink / neighbor / current mass, relative to m
 
     const bool stamp = lane == 0 && quad == 0;
-    for (int jj = wg; jj < n_kv; jj += kWG) {
+    for (int jj = wg; jj < n_kv; jj += 3) {
       const int j = kv_begin + jj;
-      const int sb = jj % 3;     // score buffer
-      const int use = jj / 3;    // use count of that buffer
-      const uint32_t tS = tmem + lane_off + sb * 128;  // S, then P in its first 64 columns
+      const int use = jj / 3;
       if (stamp) DF_STAMP(wg, use, 0);
-      mbar_wait(s_full + sb, use & 1);
+      mbar_wait(s_full + wg, use & 1);
       tc_fence_after();
       if (stamp) DF_STAMP(wg, use, 1);
       const int valid = hd.n_tok - j * kBN;  // keys of this tile inside the head's context
@@ -892,8 +890,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kWG), 1
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        arrive_leader(p_full + 2 * sb);
-        arrive_leader(p_full + 2 * sb + 1);
+        arrive_leader(p_full + 2 * wg);
+        arrive_leader(p_full + 2 * wg + 1);
       }
       continue;
 #endif
@@ -909,18 +907,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kWG), 1
         }
         tmem_wait_st();
       }
-      // kWG == 3, pass 1: the row max of the tile, 64 columns per TMEM load.  kWG == 2: the whole row
-      // into registers once (r1p), its max, then the exponentials from registers
+      // pass 1: the row max of the tile, 64 columns per TMEM load
       float mx;
-      uint32_t r1p[kWG == 2 ? 128 : 1];
-      if constexpr (kWG == 2) {
-        tmem_ld32(tS + 0, r1p);
-        tmem_ld32(tS + 32, r1p + 32);
-        tmem_ld32(tS + 64, r1p + 64);
-        tmem_ld32(tS + 96, r1p + 96);
-        tmem_wait_ld();
-        mx = row_max128(r1p);
-      } else {
+      {
         uint32_t r[64];
         tmem_ld32(tS + 0, r);
         tmem_ld32(tS + 32, r + 32);
@@ -1023,20 +1012,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kWG), 1
         next_b = (c0 / p.hw + 1) * p.hw - c0;
         kind = p.region_tab[h * p.max_slots + slot];
       }
-      uint32_t rb[kWG == 2 ? 1 : 2][32];
-      if constexpr (kWG == 3) {
-        tmem_ld32(tS, rb[0]);
-        tmem_wait_ld();
-      }
+      uint32_t rb[2][32];
+      tmem_ld32(tS, rb[0]);
+      tmem_wait_ld();
 #pragma unroll
       for (int quarter = 0; quarter < 4; ++quarter) {
-        uint32_t* r;
-        if constexpr (kWG == 2) {
-          r = r1p + quarter * 32;
-        } else {
-          r = rb[quarter & 1];
-          if (quarter < 3) tmem_ld32(tS + (quarter + 1) * 32, rb[(quarter + 1) & 1]);
-        }
+        uint32_t* r = rb[quarter & 1];
+        if (quarter < 3) tmem_ld32(tS + (quarter + 1) * 32, rb[(quarter + 1) & 1]);
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
@@ -1070,13 +1052,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kWG), 1
             }
           }
         }
-        if (kWG == 3 && quarter < 3) tmem_wait_ld();  // chunk quarter+1 is in registers
+        if (quarter < 3) tmem_wait_ld();  // chunk quarter+1 is in registers
         tmem_st16(tS + quarter * 16, pk);
         if (quarter == 1) {  // keys 0-63 of P: PV_jj may start
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) arrive_leader(p_full + 2 * sb);
+          if (lane == 0) arrive_leader(p_full + 2 * wg);
 #if DF_SCHED_FENCE
           sched_fence(p.n_heads < 0, last_flag);
 #endif
@@ -1099,15 +1081,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kWG), 1
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) arrive_leader(p_full + 2 * sb + 1);
+      if (lane == 0) arrive_leader(p_full + 2 * wg + 1);
       if (stamp) DF_STAMP(wg, use, 4);
     }
 
     // ------------------------------------------------------------ epilogue
     // every WG brings its row sum to the final running max (the last tile's WG has it), then sums
-    const int last_wg = (n_kv - 1) % kWG;
+    const int last_wg = (n_kv - 1) % 3;
     if (wg == last_wg) m_fin[row_local] = m;
-    softmax_bar_sync(kWG * 4 * 32);
+    softmax_bar_sync(12 * 32);
     {
       const float mf = m_fin[row_local];
       const float a = (l > 0.f) ? ex2(m - mf) : 0.f;  // m = -inf (no tile): l is 0 and stays 0
@@ -1120,17 +1102,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kWG), 1
       }
       m = mf;
     }
-    softmax_bar_sync(kWG * 4 * 32);
-    l = 0.f;
-#pragma unroll
-    for (int g = 0; g < kWG; ++g) l += l_x[g * 512 + row_local];
+    softmax_bar_sync(12 * 32);
+    l = l_x[row_local] + l_x[512 + row_local] + l_x[1024 + row_local];
     if constexpr (kProbe) {
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        reg_acc[k] = 0.f;
-#pragma unroll
-        for (int g = 0; g < kWG; ++g) reg_acc[k] += l_x[g * 512 + (k + 1) * 128 + row_local];
-      }
+      for (int k = 0; k < 3; ++k)
+        reg_acc[k] = l_x[(k + 1) * 128 + row_local] + l_x[512 + (k + 1) * 128 + row_local] +
+                     l_x[1024 + (k + 1) * 128 + row_local];
     }
     const int lb = (n_kv - 1) % 3;
     mbar_wait(pv_done + lb, ((n_kv - 1) / 3) & 1);  // the last PV (PVs land in order)
@@ -1139,8 +1117,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kWG), 1
     const bool row_ok = row < p.hw;
     const int64_t orow_off = (static_cast<int64_t>(hd.o_head) * p.hw + row) * p.out_ld;
     __nv_bfloat16* orow = p.out + orow_off;
-    const int c_lo = wg * (D / 2);  // WG 0 / 1 store output columns [c_lo, c_lo + 64); the last WG the probe rows
-    const bool probe_wg = wg == kWG - 1;
+    const int c_lo = wg * (D / 2);  // WG 0 / 1 store output columns [c_lo, c_lo + 64); WG 2 the probe rows
     auto store_row = [&](const float* o, int c0, float scale) {
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
@@ -1169,9 +1146,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kWG), 1
           tmem_wait_ld();
           if (row_ok) store_row(reinterpret_cast<const float*>(o), c_lo + c * 32, inv_l);
         }
-      }
-      if constexpr (kProbe) {
-        if (probe_wg && row_ok && p.row_sampled[row]) {
+      } else if constexpr (kProbe) {
+        if (row_ok && p.row_sampled[row]) {
           float* dst = p.probe_rows + (static_cast<int64_t>(h) * p.hw + row) * 3;
           dst[0] = reg_acc[0] * inv_l;
           dst[1] = reg_acc[1] * inv_l;
@@ -1196,21 +1172,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kWG), 1
                    make_float4(__uint_as_float(o[4 * v]), __uint_as_float(o[4 * v + 1]),
                                __uint_as_float(o[4 * v + 2]), __uint_as_float(o[4 * v + 3])));
         }
-      }
-      if (probe_wg) {
+      } else {
         float* my_ml = p.ws_ml + (slot_of(piece) * 2 * kBM + row_local) * 8;
         __stcg(reinterpret_cast<float4*>(my_ml), make_float4(m, l, reg_acc[0], reg_acc[1]));
         __stcg(my_ml + 4, reg_acc[2]);
       }
       __threadfence();
-      softmax_bar_sync(kWG * 4 * 32);
+      softmax_bar_sync(12 * 32);
       if (threadIdx.x == 64) {
         const int prev = atomicAdd(p.ws_cnt + group, 1);
         *last_flag = (prev == ns - 1);
         if (prev == ns - 1) p.ws_cnt[group] = 0;
         __threadfence();
       }
-      softmax_bar_sync(kWG * 4 * 32);
+      softmax_bar_sync(12 * 32);
       if (*last_flag && row_ok) {
         float M = -INFINITY;
         for (int i = 0; i < ns; ++i) M = fmaxf(M, __ldcg(p.ws_ml + (slot_of(i) * 2 * kBM + row_local) * 8));
@@ -1247,9 +1222,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kWG), 1
             }
             store_row(acc, c_lo + c * 32, inv);
           }
-        }
-        if constexpr (kProbe) {
-          if (probe_wg && p.row_sampled[row]) {
+        } else if constexpr (kProbe) {
+          if (p.row_sampled[row]) {
             float* dst = p.probe_rows + (static_cast<int64_t>(h) * p.hw + row) * 3;
             dst[0] = racc[0] * inv;
             dst[1] = racc[1] * inv;
@@ -1269,33 +1243,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads(kWG), 1
   }
 }
 
-template <bool kProbe, int kWG>
-static int launch_attn_pair_wg(const AttnParams& p, int grid, cudaStream_t stream) {
-  auto kern = df_attn_pair_kernel<kProbe, kWG>;
+template <bool kProbe>
+static int launch_attn_pair(const AttnParams& p, int grid, cudaStream_t stream) {
+  auto kern = df_attn_pair_kernel<kProbe>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg::kSmem);
     if (e != cudaSuccess) return set_cuda_error("cudaFuncSetAttribute(df_attn_pair_kernel)", e);
     configured = true;
   }
-  kern<<<grid, pair_threads(kWG), PairCfg::kSmem, stream>>>(p);
+  kern<<<grid, kPairThreads, PairCfg::kSmem, stream>>>(p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error("df_attn_pair_kernel launch", e);
   return DF_OK;
-}
-
-// softmax warpgroups of the pair kernel: DF_PAIR_WG=2 or 3 (dev A/B), default 3
-int pair_wgs() {
-  static const int n = [] {
-    const char* env = std::getenv("DF_PAIR_WG");
-    return (env && env[0] == '2') ? 2 : 3;
-  }();
-  return n;
-}
-
-template <bool kProbe>
-static int launch_attn_pair(const AttnParams& p, int grid, cudaStream_t stream) {
-  return pair_wgs() == 2 ? launch_attn_pair_wg<kProbe, 2>(p, grid, stream) : launch_attn_pair_wg<kProbe, 3>(p, grid, stream);
 }
 
 template <int D, bool kProbe>
