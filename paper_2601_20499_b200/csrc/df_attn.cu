@@ -92,6 +92,7 @@ struct __align__(64) AttnParams {
   int32_t* ws_cnt;       // [group] arrival counters (zero between launches)
   __nv_bfloat16* peer_out[DF_MAX_PEERS];  // fused all-gather: the same rows into every peer's buffer
   int32_t n_peers;
+  int32_t q_per_head;    // qmap is [head][hw][d] (rows past hw zero-fill); else [1][q_rows][d]
   int64_t out_ld;
   int32_t hw;
   int32_t d_out;
@@ -240,13 +241,14 @@ __global__ void __launch_bounds__(kThreads, 1) df_attn_kernel(const __grid_const
       prefetch_tmap(kmap);
       prefetch_tmap(vmap);
       const uint64_t keep = policy_evict_last();  // K/V re-read by every q-tile pair of the head
-      const int qrow0 = hd.q_head * p.hw + qp * 2 * kBM;
+      const int qrow0 = (p.q_per_head ? 0 : hd.q_head * p.hw) + qp * 2 * kBM;
+      const int qz = p.q_per_head ? hd.q_head : 0;
       const int nq = two ? 2 : 1;
       mbar_expect_tx(q_full, nq * C::kTileBytes);
       for (int t = 0; t < nq; ++t)
         for (int b = 0; b < C::kBoxes; ++b)
-          tma_load_2d(smem + C::kQOff + t * C::kTileBytes + b * C::kBoxBytes, &p.qmap, q_full, b * 64,
-                      qrow0 + t * kBM);
+          tma_load_3d(smem + C::kQOff + t * C::kTileBytes + b * C::kBoxBytes, &p.qmap, q_full, b * 64,
+                      qrow0 + t * kBM, qz);
       for (int jj = 0; jj < n_kv; ++jj) {
         const int row = hd.base_row + (kv_begin + jj) * kBN;
         {
@@ -758,6 +760,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     }
     fence_mbar_init();
   }
+#ifdef DF_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 1024) {
+    g_cta_time[blockIdx.x][0] = gtimer();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_cta_time[blockIdx.x][3] = smid;
+  }
+#endif
   if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   tc_fence_before();
@@ -774,11 +784,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       prefetch_tmap(kmap);
       prefetch_tmap(vmap);
       const uint64_t keep = policy_evict_last();
-      const int qrow0 = hd.q_head * p.hw + qt * 2 * kBM + static_cast<int>(crank) * kBM;
+      const int qrow0 = (p.q_per_head ? 0 : hd.q_head * p.hw) + qt * 2 * kBM + static_cast<int>(crank) * kBM;
+      const int qz = p.q_per_head ? hd.q_head : 0;
       if (crank == 0) mbar_expect_tx(q_full, 2 * C::kQBytes);
       const uint32_t lq = mapa_shared(smem_u32(q_full), 0);
       for (int b = 0; b < 2; ++b)
-        tma_load_2d_pair(smem + C::kQOff + b * C::kQBoxBytes, &p.qmap, lq, b * 64, qrow0, keep);
+        tma_load_3d_pair(smem + C::kQOff + b * C::kQBoxBytes, &p.qmap, lq, b * 64, qrow0, qz, keep);
       // K runs kKAhead tiles ahead of V (QK_{j+3} is issued right after PV_j)
       auto load_k = [&](int jj) {
         const int s = jj % C::kStagesK;
@@ -878,6 +889,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     float reg_acc[3] = {0.f, 0.f, 0.f};  // probe: sink / neighbor / current mass, relative to m
 
     const bool stamp = lane == 0 && quad == 0;
+    // A lane quadrant whose 32 query rows all lie past the head's end (the last query tile of a head:
+    // at HW 4680, 5 of its 8 quadrants) has no softmax to do: its rows' P and O are never read.  Its
+    // warps only keep the barrier protocol (the same quadrant of every WG is dead, so the m hand-off
+    // between them is skipped on both sides).
+#ifndef DF_DEAD_SKIP
+#define DF_DEAD_SKIP 1
+#endif
+    const bool dead = DF_DEAD_SKIP && qt * 2 * kBM + static_cast<int>(crank) * kBM + quad * 32 >= p.hw;
     for (int jj = wg; jj < n_kv; jj += 3) {
       const int j = kv_begin + jj;
       const int use = jj / 3;
@@ -885,6 +904,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       mbar_wait(s_full + wg, use & 1);
       tc_fence_after();
       if (stamp) DF_STAMP(wg, use, 1);
+      if (dead) {
+        __syncwarp();
+        if (lane == 0) {
+          arrive_leader(p_full + 2 * wg);
+          arrive_leader(p_full + 2 * wg + 1);
+        }
+        continue;
+      }
       const int valid = hd.n_tok - j * kBN;  // keys of this tile inside the head's context
 #ifdef DF_DIAG_NO_SOFTMAX  // dev: tensor-pipe-only timing (P = whatever TMEM holds)
       tc_fence_before();
@@ -1086,6 +1113,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     }
 
     // ------------------------------------------------------------ epilogue
+#ifdef DF_TRACE
+    if (threadIdx.x == 64 && blockIdx.x < 1024) g_cta_time[blockIdx.x][1] = gtimer();
+#endif
     // every WG brings its row sum to the final running max (the last tile's WG has it), then sums
     const int last_wg = (n_kv - 1) % 3;
     if (wg == last_wg) m_fin[row_local] = m;
@@ -1138,7 +1168,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     };
     if (ns == 1) {
       const float inv_l = 1.f / l;
-      if (wg < 2) {
+      if (wg < 2 && !dead) {
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
           uint32_t o[32];
@@ -1159,7 +1189,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       const int group = (hd.group_base + qt) * 2 + static_cast<int>(crank);
       const int64_t slot0 = static_cast<int64_t>(hd.part_base) + static_cast<int64_t>(qt) * ns;
       auto slot_of = [&](int i) { return (slot0 + i) * 2 + crank; };
-      if (wg < 2) {
+      if (dead) {
+      } else if (wg < 2) {
         float* my_o = p.ws_o + (slot_of(piece) * 2 * kBM + row_local) * D;
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
@@ -1237,6 +1268,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   tc_fence_before();
   __syncthreads();
   cluster_sync_all();  // the peer's smem and TMEM stay live until the leader's MMAs are done
+#ifdef DF_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_time[blockIdx.x][2] = gtimer();
+#endif
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc_pair(tmem, 512);
@@ -1614,7 +1648,11 @@ extern "C" int df_attn_fwd(const df_attn_args* a, void* stream) {
 
   AttnParams p;
   std::memset(&p, 0, sizeof(p));
-  rc = encode_rowmajor_bf16(&p.qmap, a->q, a->q_rows, a->head_dim);
+  // Q as [head][hw][d] when the rows are whole heads: a head's last query tile then reads zeros past
+  // its hw rows (TMA OOB fill) instead of the next head's rows -- zero operands for the padding rows
+  p.q_per_head = (a->q_rows % a->hw) == 0;
+  rc = p.q_per_head ? encode_bf16_3d(&p.qmap, a->q, a->q_rows / a->hw, a->hw, a->head_dim, 128)
+                    : encode_bf16_3d(&p.qmap, a->q, 1, a->q_rows, a->head_dim, 128);
   if (rc != DF_OK) return rc;
   std::memcpy(p.kvmap, a->kv_maps, static_cast<size_t>(a->num_arenas) * DF_MAPS_PER_ARENA * DF_TMAP_BYTES);
   p.out = static_cast<__nv_bfloat16*>(a->out);

@@ -73,6 +73,25 @@ int encode_bf16_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t col
   return DF_OK;
 }
 
+int encode_bf16_3d(CUtensorMap* map, const void* base, int64_t depth, int64_t rows, int64_t cols, int32_t box_rows) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return set_error(DF_E_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+  if (cols < 64 || cols % 8) return set_error(DF_E_SHAPE, "tensor map cols %lld", (long long)cols);
+  if (rows < 1 || depth < 1 || rows * depth > (int64_t(1) << 31))
+    return set_error(DF_E_SHAPE, "tensor map rows %lld x depth %lld", (long long)rows, (long long)depth);
+  if (box_rows < 1 || box_rows > 256) return set_error(DF_E_SHAPE, "tensor map box rows %d", box_rows);
+  if (reinterpret_cast<uintptr_t>(base) & 15) return set_error(DF_E_ARG, "tensor map base not 16-byte aligned");
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(depth)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols) * 2, static_cast<cuuint64_t>(rows * cols) * 2};
+  cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(DF_E_CUDA, "cuTensorMapEncodeTiled (3d) failed (CUresult %d)", int(r));
+  return DF_OK;
+}
+
 int encode_rowmajor_bf16(CUtensorMap* map, const void* base, int64_t rows, int32_t width, int32_t box_rows) {
   if (width != 64 && width != 128) return set_error(DF_E_SHAPE, "tensor map width %d not 64/128", width);
   return encode_bf16_2d(map, base, rows, width, width, box_rows);

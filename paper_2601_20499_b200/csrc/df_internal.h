@@ -22,6 +22,9 @@ int encode_rowmajor_bf16(CUtensorMap* map, const void* base, int64_t rows, int32
 // SWIZZLE_128B, OOB -> zero.
 int encode_bf16_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int32_t box_rows);
 
+// bf16 [depth][rows][cols] (contiguous), box = box_rows x 64 columns x 1, SWIZZLE_128B, OOB -> zero.
+int encode_bf16_3d(CUtensorMap* map, const void* base, int64_t depth, int64_t rows, int64_t cols, int32_t box_rows);
+
 // Multiprocessor count of the current device (148 on B200), cached.
 int sm_count_cached();
 

@@ -94,6 +94,9 @@ struct ProjParams {
 // x 128 B per warp instruction.  Issued one chunk ahead of its use -- the first chunk of a tile
 // before the accumulator is ready -- so the epilogue does not stall on HBM latency per chunk.
 __device__ __forceinline__ void load_residual(const ProjParams& p, int lane, int row0, int n0, float4 (&xv)[8]) {
+#if defined(DF_DIAG_OPROJ_NOLOAD) || defined(DF_DIAG_OPROJ_NOEPI)
+  return;  // dev: epilogue cost diagnostics (wrong results)
+#endif
   if (n0 >= p.n) return;
   const int piece = lane & 7;
 #pragma unroll
@@ -151,7 +154,11 @@ __device__ __forceinline__ void epilogue_chunk(const ProjParams& p, uint8_t* stg
       srow[i] = make_float4(__uint_as_float(r[4 * i + 0]), __uint_as_float(r[4 * i + 1]),
                             __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
     __syncwarp();
+#ifdef DF_DIAG_OPROJ_NOEPI
+    if (false) {
+#else
     if (n0 < p.n) {
+#endif
       const int piece = lane & 7;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {

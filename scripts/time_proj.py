@@ -62,3 +62,19 @@ def unfused():
         kd[h].copy_(y[:, 1, h])
         vd[h].copy_(y[:, 2, h])
 print(f"cuBLAS + scatter copies (unfused qkv) {timeit(unfused):.1f} us")
+
+# out-projection with cold operands: 8 rotating (o, x, x_bf16) sets (8 x 58 MB > L2), as in the 30-layer step
+sets = [(torch.randn(H, hw, d, device=dev).to(torch.bfloat16), torch.randn(hw, D, device=dev),
+         torch.empty(hw, D, dtype=torch.bfloat16, device=dev)) for _ in range(8)]
+for bn in ("192", "256", None):
+    if bn:
+        os.environ["DF_PROJ_BN"] = bn
+    else:
+        os.environ.pop("DF_PROJ_BN", None)
+    ls = [K.prepare_out_projection(o_, wo, x_, xb_, d) for o_, x_, xb_ in sets]
+    i = [0]
+    def step():
+        ls[i[0] % 8].launch()
+        i[0] += 1
+    t = timeit(step, reps=80)
+    print(f"cold out-proj BN={bn or 'auto'}: {t:.1f} us {2 * hw * D * D / t / 1e6:.0f} TFLOP/s")

@@ -77,6 +77,52 @@ def test_stale_rows_and_masked_tails(scale_q, pair):
         assert err <= 2e-2, (h, err)
 
 
+@pytest.mark.parametrize("pair", [False, True])
+def test_running_max_jumps_inside_later_tiles(pair):
+    """Logit spikes placed in a later kv tile's first half, its second half, and tiles after a jump:
+    the CTA pair's single-pass softmax must fall back (first half: two-pass redo; second half: O and
+    the row sum rescaled after the first-half PV) and the next warpgroups must pick up the moved m."""
+    from paper_2601_20499_b200 import kernels as K
+
+    torch.manual_seed(7)
+    dev = torch.device("cuda:0")
+    hw, width = 256, 128
+    ctx = 128 * 16
+    spikes = [  # per head: (key index, logit in nats along the shared direction)
+        [(128 * 4 + 10, 30.0), (128 * 7 + 100, 60.0), (128 * 9 + 3, 90.0)],
+        [(128 * 5 + 70, 25.0), (128 * 6 + 127, 50.0), (128 * 13 + 64, 75.0)],
+        [(128 * 3 + 64, 40.0), (128 * 3 + 65, 41.0), (128 * 11 + 1, 80.0)],
+    ]
+    H = len(spikes)
+    arena = K.KVArena(H * K.KVArena.region_rows(ctx), width, dev)
+    u = torch.randn(width, device=dev)
+    u = u / u.norm()
+    # q rows: the shared direction plus per-row noise (rows differ in where their own max lands)
+    qf = u[None, :] * 4.0 + 0.3 * torch.randn(H * hw, width, device=dev)
+    q = qf.to(torch.bfloat16)
+    scale = 1.0 / math.sqrt(width)
+    work = []
+    for h, sp in enumerate(spikes):
+        base = arena.allocate(ctx)
+        k = torch.randn(ctx, width, device=dev)
+        for key, logit in sp:
+            k[key] += u * (logit / (4.0 * scale))
+        arena.k[base:base + ctx] = k.to(torch.bfloat16)
+        arena.v[base:base + ctx] = torch.randn(ctx, width, device=dev).to(torch.bfloat16)
+        work.append(K.HeadWork(arena, base, ctx, h, h))
+    out = torch.zeros(H * hw, width, device=dev, dtype=torch.bfloat16)
+    K.attention(q, out, work, hw, scale, pair=pair)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+    for h, w in enumerate(work):
+        kk = arena.k[w.base_row:w.base_row + ctx].double()
+        vv = arena.v[w.base_row:w.base_row + ctx].double()
+        ref = torch.softmax((q[h * hw:(h + 1) * hw].double() @ kk.T) * scale, dim=-1) @ vv
+        got = out[h * hw:(h + 1) * hw].double()
+        err = (got - ref).abs().max().item() / ref.abs().max().item()
+        assert err <= 2e-2, (h, err)
+
+
 def test_probe_region_masses_with_split_kv():
     """DF_ATTN_PROBE on a launch the planner splits (2 heads, 94 kv tiles, 4 items on 148 SMs):
     the combine merges O, l and the three region masses of every piece (profiler.py:118-129)."""
