@@ -53,6 +53,7 @@ constexpr int kThreads = kWarps * 32;
 #define DF_RESCALE_THRESHOLD 16.0f  // P <= 2^16 of the running reference; measured: 8 -> 16 cuts N(0,3) logits 352 -> 342 us, N(0,6) 373 -> 350
 #endif
 constexpr float kRescaleThreshold = DF_RESCALE_THRESHOLD;  // log2 units
+constexpr int kMaxSplit = 16;  // kv pieces per query tile (split-KV)
 #ifndef DF_EMU_NUM
 #define DF_EMU_NUM 1
 #endif
@@ -1218,37 +1219,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       }
       softmax_bar_sync(12 * 32);
       if (*last_flag && row_ok) {
+        // the combine issues every piece's (m, l) at once and the O partials two pieces at a time
+        // (16 float4 loads in flight per thread): it is latency-bound, not bandwidth-bound
+        float ei[kMaxSplit], li[kMaxSplit];
         float M = -INFINITY;
-        for (int i = 0; i < ns; ++i) M = fmaxf(M, __ldcg(p.ws_ml + (slot_of(i) * 2 * kBM + row_local) * 8));
+#pragma unroll
+        for (int i = 0; i < kMaxSplit; ++i)
+          if (i < ns) {
+            const float4 ml = __ldcg(reinterpret_cast<const float4*>(p.ws_ml + (slot_of(i) * 2 * kBM + row_local) * 8));
+            ei[i] = ml.x;
+            li[i] = ml.y;
+            M = fmaxf(M, ml.x);
+          }
         float den = 0.f;
         float racc[3] = {0.f, 0.f, 0.f};
-        for (int i = 0; i < ns; ++i) {
-          const float* ml = p.ws_ml + (slot_of(i) * 2 * kBM + row_local) * 8;
-          const float ei = ex2(__ldcg(ml) - M);
-          den += ei * __ldcg(ml + 1);
-          if constexpr (kProbe) {
-            racc[0] += ei * __ldcg(ml + 2);
-            racc[1] += ei * __ldcg(ml + 3);
-            racc[2] += ei * __ldcg(ml + 4);
+#pragma unroll
+        for (int i = 0; i < kMaxSplit; ++i)
+          if (i < ns) {
+            ei[i] = ex2(ei[i] - M);
+            den += ei[i] * li[i];
+            if constexpr (kProbe) {
+              const float* ml = p.ws_ml + (slot_of(i) * 2 * kBM + row_local) * 8;
+              racc[0] += ei[i] * __ldcg(ml + 2);
+              racc[1] += ei[i] * __ldcg(ml + 3);
+              racc[2] += ei[i] * __ldcg(ml + 4);
+            }
           }
-        }
         const float inv = 1.f / den;
         if (wg < 2) {
-#pragma unroll 1
+#pragma unroll
           for (int c = 0; c < D / 64; ++c) {
             float acc[32];
 #pragma unroll
             for (int q = 0; q < 32; ++q) acc[q] = 0.f;
-            for (int i = 0; i < ns; ++i) {
-              const float ei = ex2(__ldcg(p.ws_ml + (slot_of(i) * 2 * kBM + row_local) * 8) - M);
-              const float* src = p.ws_o + (slot_of(i) * 2 * kBM + row_local) * D + c_lo + c * 32;
 #pragma unroll
-              for (int v = 0; v < 8; ++v) {
-                const float4 x = __ldcg(reinterpret_cast<const float4*>(src + v * 4));
-                acc[4 * v + 0] += ei * x.x;
-                acc[4 * v + 1] += ei * x.y;
-                acc[4 * v + 2] += ei * x.z;
-                acc[4 * v + 3] += ei * x.w;
+            for (int i = 0; i < kMaxSplit; i += 2) {
+              if (i < ns) {
+                const bool two = i + 1 < ns;
+                const float4* sa =
+                    reinterpret_cast<const float4*>(p.ws_o + (slot_of(i) * 2 * kBM + row_local) * D + c_lo + c * 32);
+                const float4* sb = reinterpret_cast<const float4*>(
+                    p.ws_o + (slot_of(two ? i + 1 : i) * 2 * kBM + row_local) * D + c_lo + c * 32);
+                float4 xa[8], xb[8];
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                  xa[v] = __ldcg(sa + v);
+                  xb[v] = two ? __ldcg(sb + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                const float ea = ei[i], eb = two ? ei[i + 1] : 0.f;
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                  acc[4 * v + 0] += ea * xa[v].x + eb * xb[v].x;
+                  acc[4 * v + 1] += ea * xa[v].y + eb * xb[v].y;
+                  acc[4 * v + 2] += ea * xa[v].z + eb * xb[v].z;
+                  acc[4 * v + 3] += ea * xa[v].w + eb * xb[v].w;
+                }
               }
             }
             store_row(acc, c_lo + c * 32, inv);
@@ -1343,7 +1368,6 @@ const double kSplitOverhead = env_or("DF_PLAN_SPLIT", 1.0);
 // scripts/plan_sweep.py: Wan all-context 880 -> 804 us, packed unchanged)
 const double kCombinePerPiece = env_or("DF_PLAN_COMBINE", 1.0);
 constexpr double kSingleTileFactor = 0.95;  // last pair with only its first tile valid: no ping-pong, ~as slow as a full pair (clock64 trace)
-constexpr int kMaxSplit = 16;
 const bool kPlanRefine = env_or("DF_PLAN_REFINE", 1.0) != 0.0;  // dev A/B
 
 struct Plan {
