@@ -301,6 +301,42 @@ def test_wan_layer_full_size_properties():
         assert (o_p[h].float() - ref).abs().max() / ref.abs().max() <= TOL
 
 
+def test_wan_layer_every_head_every_row_matches_oracle():
+    """BASELINE config 1 at full size against the oracle (engine.py:87-98 in fp64 on the same bf16
+    operands): every head and every one of the 4680 query rows of a warm Wan layer, all-context
+    (the planner splits one head into kv pieces: the in-kernel combine at the Wan shape) and packed
+    6 dummy / 3 sink / 3 neighbor (the padding quadrants of each head's last query tile skipped)."""
+    H, HW, d, W = 12, 4680, 128, 6
+    cfg = df.SessionConfig(num_layers=1, num_heads=H, head_dim=d, HW=HW, window_len=W, ar_steps=8, dummy_count=6)
+    g = torch.Generator(device=DEV).manual_seed(3)
+    frames = {(h, f): (torch.randn(HW, d, device=DEV, generator=g).to(torch.bfloat16),
+                       torch.randn(HW, d, device=DEV, generator=g).to(torch.bfloat16)) for h in range(H) for f in range(8)}
+    base = []
+    for h in range(H):
+        c = df.HeadKVCache(df.baseline_policy(cfg))
+        for f in range(7):
+            c.append_and_evict(df.FrameBlock(f, *frames[(h, f)]))
+        base.append(c)
+    q = (torch.randn(H, HW, d, device=DEV, generator=g) * 1.5).to(torch.bfloat16)
+    cur = [df.FrameBlock(7, *frames[(h, 7)]) for h in range(H)]
+    classes = [df.HeadClass.DUMMY] * 6 + [df.HeadClass.SINK] * 3 + [df.HeadClass.NEIGHBOR] * 3
+    out_b, _ = df.baseline_step(q, base, cur, cfg)
+    pruned = df.rebuild_caches(base, [df.derive_policy(c, cfg) for c in classes])
+    out_p, _ = df.packed_step(q, pruned, cur, classes, cfg)
+    torch.cuda.synchronize()
+    qn = q.float().cpu().numpy().astype(np.float64)
+    for caches, out in ((base, out_b), (pruned, out_p)):
+        worst = 0.0
+        for h in range(H):
+            k, v, _ = caches[h].gather_context(cur[h])
+            ref = O.batched_attention(qn[h][None], k.float().cpu().numpy().astype(np.float64)[None],
+                                      v.float().cpu().numpy().astype(np.float64)[None], 1 / math.sqrt(d))[0]
+            err = normwise(out[h][None], ref[None])[0]
+            worst = max(worst, err)
+            assert err <= TOL, (h, err)
+        assert worst <= TOL
+
+
 def test_batched_step_streams_in_one_launch():
     """batched_step (BASELINE configs[4]: several streams on one GPU): a packed, an hma and a baseline
     request from three sessions (three arenas) in one FMHA launch; every request's outputs match its own
