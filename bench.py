@@ -433,6 +433,10 @@ def kernel_configs(df, dev, bf16_peak):
         for _ in range(3):
             for l in launches:
                 l.launch(None)
+        # burst conditions for every config: let the clocks recover from the previous (possibly
+        # power-capped) measurement, e.g. the 13 hi-res all-context launches before the C5 one
+        torch.cuda.synchronize()
+        time.sleep(0.5)
         ts = []
         for _ in range(10):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
