@@ -1031,7 +1031,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       const float2 negm2 = make_float2(-m, -m);
       float2 sum2 = make_float2(0.f, 0.f);
       float span = 0.f;
-      float2 lo2 = make_float2(0.f, 0.f);
+      float2 lo2 = make_float2(0.f, 0.f), part2 = make_float2(0.f, 0.f);  // probe: keys left of the boundary
       int next_b = 0, kind = 0, slot = 0;
       const bool wide = p.hw >= kBN;
       if constexpr (kProbe) {
@@ -1061,9 +1061,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           sum2 = add2(sum2, e);
           pk[i] = pack_bf16x2(e.x, e.y);
           if constexpr (kProbe) {
-            if (wide) {
-              lo2 = add2(lo2, make_float2(c < next_b ? e.x : 0.f, c + 1 < next_b ? e.y : 0.f));
-            } else {
+            if (!wide) {
 #pragma unroll
               for (int k2 = 0; k2 < 2; ++k2) {
                 if (c + k2 == next_b) {
@@ -1076,6 +1074,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                   kind = p.region_tab[h * p.max_slots + slot];
                 }
                 span += k2 ? e.y : e.x;
+              }
+            }
+          }
+        }
+        if constexpr (kProbe) {
+          // one slot boundary at most per tile (HW >= 128): the mass left of it is the running sum after
+          // the last quarter wholly left of it, plus -- in the quarter the boundary cuts (about one tile
+          // in HW/128) -- that quarter's keys left of it, their exponentials recomputed (same code path,
+          // so lo + hi = the tile's sum)
+          if (wide) {
+            if ((quarter + 1) * 32 <= next_b) {
+              lo2 = sum2;
+            } else if (quarter * 32 < next_b) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const int c = quarter * 32 + 2 * i;
+                const float2 x =
+                    fma2(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), scale2, negm2);
+                const float2 e = emulated_pair(c / 2) ? exp2_poly2(x, p.exp_unit) : make_float2(ex2(x.x), ex2(x.y));
+                part2 = add2(part2, make_float2(c < next_b ? e.x : 0.f, c + 1 < next_b ? e.y : 0.f));
               }
             }
           }
@@ -1094,7 +1112,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       }
       if constexpr (kProbe) {
         if (wide) {
-          const float lo = lo2.x + lo2.y, hi = (sum2.x + sum2.y) - lo;
+          const float lo = (lo2.x + lo2.y) + (part2.x + part2.y), hi = (sum2.x + sum2.y) - lo;
           const int kind1 = p.region_tab[h * p.max_slots + min(slot + 1, p.max_slots - 1)];
           reg_acc[0] += (kind == 0 ? lo : 0.f) + (kind1 == 0 ? hi : 0.f);
           reg_acc[1] += (kind == 1 ? lo : 0.f) + (kind1 == 1 ? hi : 0.f);
