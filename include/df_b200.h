@@ -91,7 +91,9 @@ typedef struct df_head_desc {
 } df_head_desc;
 
 typedef struct df_attn_args {
-  const void* q;          /* device bf16 [q_rows][head_dim] */
+  const void* q;          /* device bf16 [q_rows][head_dim]; when q_rows is a multiple of hw it is
+                             read as [q_rows/hw][hw][head_dim], so a head's last query tile never
+                             touches the next head's rows (padding rows read as zeros) */
   int64_t q_rows;
   void* out;              /* device bf16; element (o_head*hw + r, c) at out[(o_head*hw+r)*out_ld + c] */
   int64_t out_ld;         /* elements */
